@@ -1,0 +1,35 @@
+// B200 executor: runs one scheduler BatchPlan per call on one GPU.
+//
+// Owns the model weights, the paged KV pool (GPU-resident block tables with a
+// device free list), the pinned host swap pool, the token history and the
+// CUDA streams.  Plans are enqueued asynchronously: the scheduler never waits
+// on the GPU because interceptions fire on decode counts, not token values
+// (reference engine.cpp:466-481), so sampled ids stay on the device.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+
+#include "../sched/scheduler.hpp"
+
+namespace ib2 {
+
+class B200Executor : public PlanSink {
+ public:
+  static std::unique_ptr<B200Executor> create(const std::string& model_json, int device,
+                                              const std::string& pools_json);
+  ~B200Executor() override = default;
+
+  void consume(const isim_batch_plan& plan) override = 0;
+  virtual void sync() = 0;
+  virtual std::string stats_json() const = 0;
+  virtual std::int32_t last_tokens(std::int32_t* out, std::int32_t cap) const = 0;
+  virtual std::int64_t last_logits(float* out, std::int64_t cap) const = 0;
+  virtual std::int32_t block_table(std::int64_t request_id, std::int32_t* out, std::int32_t cap) const = 0;
+  virtual std::int64_t free_blocks() const = 0;
+  virtual void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out,
+                       std::int64_t cap) const = 0;
+};
+
+}  // namespace ib2
