@@ -179,6 +179,16 @@ isim_status isim_session_counters(const isim_session* s, int64_t* completed, int
 isim_status isim_session_finish(isim_session* s, isim_result** out);
 void isim_session_free(isim_session* s);
 
+/* ---- Part 2d: kernel test hook ------------------------------------------- */
+
+/* K3 projection GEMM on caller device pointers: C = A[M][K] . W[N][K]^T with
+ * epilogue epi (0 store bf16 (+bias), 1 gelu(acc+bias) bf16, 2 fp32 residual
+ * add (+bias), 3 SwiGLU pairs -> bf16 [M][N/2], 4 store fp32 (+bias)).
+ * force_simt=1 runs the CUDA-core kernel instead of tcgen05. stream may be 0. */
+isim_status isim_debug_gemm(const void* a, const void* w, int32_t M, int32_t N, int32_t K, int32_t epi,
+                            const void* bias, void* out, int32_t ldo, void* outf, int32_t ldf, int32_t force_simt,
+                            void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

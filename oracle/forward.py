@@ -1,0 +1,281 @@
+"""CPU numerical oracle of the B200 model step (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may import
+this module, and only as the checker.  The product path never calls it.
+
+Parity status: *unpinned* for model arithmetic.  The reference (interceptsim)
+has no model -- its model step is the analytic CostModel::t_fwd
+(proj/include/interceptsim/cost_model.hpp:33-37, called at
+proj/src/engine.cpp:460) -- so there are no logits or token ids to pin against.
+This module restates the forward the executor runs, in float32 numpy with the
+same bf16 rounding points (GEMM inputs, q/k/v, attention output, KV cache), and
+consumes the very BatchPlans the scheduler emits.  The *scheduling* that
+produces those plans is pinned bit-exactly against the reference itself
+(oracle/_ref, see tests/test_sched_parity.py).
+
+Semantics restated:
+  * token ids: synthetic ids for prompt / API-returned positions are
+    mix64(mix64(token_seed + C*(rid+1)) + pos) % V (same hash as the device);
+    a sampling row at position p writes the greedy id for position p+1;
+  * a row at position p attends over keys [0, p] of its request (causal);
+  * KV of a position is written once per (re)computation; swaps move bytes.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def mix64(z: np.ndarray) -> np.ndarray:
+    z = np.asarray(z, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = z ^ (z >> np.uint64(30))
+        z = z * np.uint64(0xBF58476D1CE4E5B9)
+        z = z ^ (z >> np.uint64(27))
+        z = z * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def synth_weight(seed: int, tensor_id: int, count: int) -> np.ndarray:
+    """Device init kernel restated: exec/common.cuh synth_weight."""
+    with np.errstate(over="ignore"):
+        base = mix64(np.uint64((seed + 0x9E3779B97F4A7C15 * (tensor_id + 1)) & 0xFFFFFFFFFFFFFFFF))
+        h = mix64(base + np.arange(count, dtype=np.uint64))
+    u24 = (h >> np.uint64(40)).astype(np.float32)
+    u = u24 * np.float32(1.1920928955078125e-07) - np.float32(1.0)
+    return u * np.float32(0.034641016)
+
+
+def synth_token(seed: int, rid: int, pos, vocab: int):
+    with np.errstate(over="ignore"):
+        base = mix64(np.uint64((seed + 0xD1B54A32D192ED03 * (rid + 1)) & 0xFFFFFFFFFFFFFFFF))
+        return (mix64(base + np.asarray(pos, dtype=np.uint64)) % np.uint64(vocab)).astype(np.int64)
+
+
+def bf16(x: np.ndarray) -> np.ndarray:
+    """Round float32 to bfloat16 (nearest-even), returned as float32."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    r = ((u >> np.uint32(16)) & np.uint32(1)) + np.uint32(0x7FFF)
+    with np.errstate(over="ignore"):
+        return ((u + r) & np.uint32(0xFFFF0000)).view(np.float32)
+
+
+PRESETS = {
+    "tiny": dict(family="gpt2", layers=2, d_model=256, heads=4, ffn=1024, vocab=4096, rotary_dim=0),
+    "gptj-6b": dict(family="gptj", layers=28, d_model=4096, heads=16, ffn=16384, vocab=50400, rotary_dim=64),
+    "vicuna-13b": dict(family="llama", layers=40, d_model=5120, heads=40, ffn=13824, vocab=32000, rotary_dim=128),
+}
+
+
+class ModelOracle:
+    """Weights + forward of one model (exec/model.cpp layout_weights order)."""
+
+    def __init__(self, spec: dict):
+        s = dict(PRESETS[spec.get("preset", "tiny")])
+        s.update({k: v for k, v in spec.items() if k != "preset"})
+        s.setdefault("max_pos", 4160)
+        s.setdefault("weight_seed", 1234)
+        s.setdefault("token_seed", 99)
+        s.setdefault("norm_eps", 1e-6 if s["family"] == "llama" else 1e-5)
+        self.s = s
+        self.fam = s["family"]
+        self.L, self.D, self.H, self.F, self.V = s["layers"], s["d_model"], s["heads"], s["ffn"], s["vocab"]
+        self.hd = self.D // self.H
+        self.rot = s["rotary_dim"]
+        self._next_id = 0
+        D, F, V = self.D, self.F, self.V
+        bias = self.fam != "llama"
+        self.tok_emb = self._put(V * D, 0).reshape(V, D)
+        self.pos_emb = self._put(s["max_pos"] * D, 0).reshape(s["max_pos"], D) if self.fam == "gpt2" else None
+        self.layers = []
+        for _ in range(self.L):
+            lw = {}
+            lw["ln1_g"] = self._put(D, 1)
+            lw["ln1_b"] = self._put(D, 2) if bias else None
+            if self.fam != "gptj":
+                lw["ln2_g"] = self._put(D, 1)
+                lw["ln2_b"] = self._put(D, 2) if bias else None
+            lw["w_qkv"] = self._put(3 * D * D, 0).reshape(3 * D, D)
+            lw["b_qkv"] = self._put(3 * D, 0) if self.fam == "gpt2" else None
+            lw["w_o"] = self._put(D * D, 0).reshape(D, D)
+            lw["b_o"] = self._put(D, 0) if self.fam == "gpt2" else None
+            fin = 2 * F if self.fam == "llama" else F
+            lw["w_in"] = self._put(fin * D, 0).reshape(fin, D)
+            lw["b_in"] = self._put(F, 0) if bias else None
+            lw["w_out"] = self._put(D * F, 0).reshape(D, F)
+            lw["b_out"] = self._put(D, 0) if bias else None
+            self.layers.append(lw)
+        self.lnf_g = self._put(D, 1)
+        self.lnf_b = self._put(D, 2) if bias else None
+        self.lm_w = self._put(V * D, 0).reshape(V, D)
+        self.lm_b = self._put(V, 0) if self.fam == "gptj" else None
+        if self.rot:
+            half = self.rot // 2
+            pos = np.arange(s["max_pos"], dtype=np.float64)[:, None]
+            inv = np.array([math.pow(10000.0, -2.0 * i / self.rot) for i in range(half)])
+            ang = pos * inv[None, :]
+            self.cos = np.cos(ang).astype(np.float32)
+            self.sin = np.sin(ang).astype(np.float32)
+
+    def _put(self, count: int, kind: int) -> np.ndarray:
+        tid = self._next_id
+        self._next_id += 1
+        if kind == 1:
+            return np.ones(count, np.float32)
+        if kind == 2:
+            return np.zeros(count, np.float32)
+        return bf16(synth_weight(self.s["weight_seed"], tid, count))
+
+    # ---- pieces ---------------------------------------------------------------
+    def norm(self, x, g, b):
+        x = x.astype(np.float32)
+        if self.fam == "llama":
+            var = np.mean(x * x, axis=-1, keepdims=True, dtype=np.float32)
+            y = x * (np.float32(1.0) / np.sqrt(var + np.float32(self.s["norm_eps"]))) * g
+        else:
+            mu = np.mean(x, axis=-1, keepdims=True, dtype=np.float32)
+            d = x - mu
+            var = np.mean(d * d, axis=-1, keepdims=True, dtype=np.float32)
+            y = d * (np.float32(1.0) / np.sqrt(var + np.float32(self.s["norm_eps"]))) * g
+            if b is not None:
+                y = y + b
+        return bf16(y.astype(np.float32))
+
+    @staticmethod
+    def lin(x, w, b=None):
+        y = (x.astype(np.float32) @ w.T.astype(np.float32)).astype(np.float32)
+        return y + b if b is not None else y
+
+    def rope(self, t, pos):
+        """t: [n, H, hd] bf16-valued float32; rotated in float32, re-rounded."""
+        if not self.rot:
+            return t
+        half = self.rot // 2
+        c = self.cos[pos][:, None, :]
+        s = self.sin[pos][:, None, :]
+        t = t.copy()
+        if self.fam == "gptj":
+            a, b = t[..., 0:self.rot:2].copy(), t[..., 1:self.rot:2].copy()
+            t[..., 0:self.rot:2] = a * c - b * s
+            t[..., 1:self.rot:2] = b * c + a * s
+        else:
+            a, b = t[..., :half].copy(), t[..., half:self.rot].copy()
+            t[..., :half] = a * c - b * s
+            t[..., half:self.rot] = b * c + a * s
+        return bf16(t)
+
+
+class ForwardOracle:
+    """Replays BatchPlans (dicts from the scheduler's plan log) on the CPU."""
+
+    def __init__(self, model_spec: dict):
+        self.m = ModelOracle(model_spec)
+        self.hist = {}     # rid -> int64[ctx]
+        self.kv = {}       # rid -> float32[L, cap, 2, D] (bf16 values)
+
+    def _ensure(self, rid, upto):
+        L, D = self.m.L, self.m.D
+        if rid not in self.hist:
+            self.hist[rid] = np.zeros(max(64, upto + 1), np.int64)
+            self.kv[rid] = np.zeros((L, max(64, upto), 2, D), np.float32)
+        if self.hist[rid].shape[0] < upto + 1:
+            h = np.zeros(max(upto + 1, 2 * self.hist[rid].shape[0]), np.int64)
+            h[: self.hist[rid].shape[0]] = self.hist[rid]
+            self.hist[rid] = h
+        if self.kv[rid].shape[1] < upto:
+            k = np.zeros((L, max(upto, 2 * self.kv[rid].shape[1]), 2, D), np.float32)
+            k[:, : self.kv[rid].shape[1]] = self.kv[rid]
+            self.kv[rid] = k
+
+    def step(self, plan: dict, teacher_tokens=None) -> dict:
+        """Run one plan; returns {"logits": [S, V], "tokens": [S], "margin": [S]}.
+
+        teacher_tokens: tokens the device sampled (one per sampling span, in
+        span order); they overwrite the oracle's own ids in the history so
+        both sides continue from identical inputs (ties stay harmless)."""
+        m = self.m
+        D, H, hd, V = m.D, m.H, m.hd, m.V
+        for (rid, kind, _phase, lo, hi) in plan["ops"]:
+            if kind == 5:  # release
+                self.hist.pop(rid, None)
+                self.kv.pop(rid, None)
+        rows_rid, rows_pos, sample_rows, spans = [], [], [], []
+        for (rid, pos, count, kind, sample) in plan["spans"]:
+            self._ensure(rid, pos + count + 1)
+            r0 = len(rows_rid)
+            for k in range(count):
+                rows_rid.append(rid)
+                rows_pos.append(pos + k)
+            if kind == 1:  # fresh: synthetic ids
+                self.hist[rid][pos:pos + count] = synth_token(m.s["token_seed"], rid, np.arange(pos, pos + count), V)
+            spans.append((rid, pos, count, r0))
+            if sample:
+                sample_rows.append(r0 + count - 1)
+        n = len(rows_rid)
+        if n == 0:
+            return {"logits": np.zeros((0, V), np.float32), "tokens": [], "margin": []}
+        pos_arr = np.array(rows_pos)
+        toks = np.array([self.hist[r][p] for r, p in zip(rows_rid, rows_pos)])
+        x = m.tok_emb[toks].astype(np.float32)
+        if m.pos_emb is not None:
+            x = x + m.pos_emb[pos_arr]
+        scale = np.float32(1.0 / math.sqrt(hd))
+        for li, lw in enumerate(m.layers):
+            xn = m.norm(x, lw["ln1_g"], lw["ln1_b"])
+            qkv = bf16(m.lin(xn, lw["w_qkv"], lw["b_qkv"]))
+            q = m.rope(qkv[:, :D].reshape(n, H, hd), pos_arr)
+            k = m.rope(qkv[:, D:2 * D].reshape(n, H, hd), pos_arr)
+            v = qkv[:, 2 * D:].reshape(n, H, hd)
+            for (rid, pos, count, r0) in spans:
+                self.kv[rid][li, pos:pos + count, 0] = k[r0:r0 + count].reshape(count, D)
+                self.kv[rid][li, pos:pos + count, 1] = v[r0:r0 + count].reshape(count, D)
+            attn = np.zeros((n, D), np.float32)
+            for (rid, pos, count, r0) in spans:
+                K = self.kv[rid][li, : pos + count, 0].reshape(-1, H, hd)
+                Vv = self.kv[rid][li, : pos + count, 1].reshape(-1, H, hd)
+                qq = q[r0:r0 + count]                       # [c, H, hd]
+                s = np.einsum("chd,khd->hck", qq, K).astype(np.float32) * scale
+                kpos = np.arange(pos + count)
+                qpos = pos + np.arange(count)
+                s = np.where(kpos[None, None, :] <= qpos[None, :, None], s, -np.inf)
+                s = s - s.max(axis=-1, keepdims=True)
+                p = np.exp(s).astype(np.float32)
+                p = p / p.sum(axis=-1, keepdims=True)
+                o = np.einsum("hck,khd->chd", p, Vv).astype(np.float32)
+                attn[r0:r0 + count] = o.reshape(count, D)
+            attn = bf16(attn)
+            if m.fam == "gptj":
+                x = x + m.lin(attn, lw["w_o"], lw["b_o"])
+                u = m.lin(xn, lw["w_in"], lw["b_in"])
+                u = bf16(_gelu(u))
+                x = x + m.lin(u, lw["w_out"], lw["b_out"])
+            else:
+                x = x + m.lin(attn, lw["w_o"], lw["b_o"])
+                xn2 = m.norm(x, lw["ln2_g"], lw["ln2_b"])
+                if m.fam == "llama":
+                    gu = m.lin(xn2, lw["w_in"])
+                    g, u = gu[:, 0::2], gu[:, 1::2]
+                    h = bf16((g / (np.float32(1) + np.exp(-g))) * u)
+                else:
+                    h = bf16(_gelu(m.lin(xn2, lw["w_in"], lw["b_in"])))
+                x = x + m.lin(h, lw["w_out"], lw["b_out"])
+        if not sample_rows:
+            return {"logits": np.zeros((0, V), np.float32), "tokens": [], "margin": []}
+        xs = m.norm(x[sample_rows], m.lnf_g, m.lnf_b)
+        logits = m.lin(xs, m.lm_w, m.lm_b).astype(np.float32)
+        top2 = np.sort(logits, axis=-1)[:, -2:]
+        toks_out = np.argmax(logits, axis=-1)
+        margin = top2[:, 1] - top2[:, 0]
+        chosen = teacher_tokens if teacher_tokens is not None else toks_out
+        for i, r in enumerate(sample_rows):
+            self.hist[rows_rid[r]][rows_pos[r] + 1] = int(chosen[i])
+        return {"logits": logits, "tokens": toks_out.tolist(), "margin": margin.tolist()}
+
+
+def _gelu(v: np.ndarray) -> np.ndarray:
+    v = v.astype(np.float32)
+    return (np.float32(0.5) * v * (np.float32(1.0) + np.tanh(np.float32(0.7978845608028654) *
+                                                           (v + np.float32(0.044715) * v * v * v)))).astype(np.float32)

@@ -1,0 +1,96 @@
+// Device-side vocabulary shared by the executor's kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../sched/base.hpp"
+
+namespace ib2 {
+
+using bf16 = __nv_bfloat16;
+
+#define IB2_CUDA(expr)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      throw ::ib2::DeviceError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " @" __FILE__); \
+  } while (0)
+
+#define IB2_LAUNCH_CHECK() IB2_CUDA(cudaGetLastError())
+
+constexpr int kBlockTokens = 16;  // paged KV block = 16 token positions
+
+// splitmix64 finalizer: the counter hash behind synthetic weights and ids.
+__host__ __device__ inline std::uint64_t mix64(std::uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xbf58476d1ce4e5b9ULL;
+  z ^= z >> 27;
+  z *= 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// Uniform weight with std 0.02: u in [-1,1) on a 2^-23 grid times 0.02*sqrt(3).
+__host__ __device__ inline float synth_weight(std::uint64_t seed, std::uint32_t tensor_id, std::uint64_t idx) {
+  const std::uint64_t base = mix64(seed + 0x9E3779B97F4A7C15ULL * (static_cast<std::uint64_t>(tensor_id) + 1));
+  const std::uint32_t u24 = static_cast<std::uint32_t>(mix64(base + idx) >> 40);
+  const float u = static_cast<float>(u24) * 1.1920928955078125e-07f - 1.0f;
+  return u * 0.034641016f;
+}
+
+// Synthetic prompt / API-returned token id at a position of a request.
+__host__ __device__ inline std::int32_t synth_token(std::uint64_t seed, std::int64_t req_id, std::int64_t pos,
+                                                   std::int32_t vocab) {
+  const std::uint64_t base = mix64(seed + 0xD1B54A32D192ED03ULL * static_cast<std::uint64_t>(req_id + 1));
+  return static_cast<std::int32_t>(mix64(base + static_cast<std::uint64_t>(pos)) % static_cast<std::uint64_t>(vocab));
+}
+
+// One query row of the batch.
+struct RowDesc {
+  std::int32_t slot;
+  std::int32_t pos;
+  std::int32_t synthetic;  // 1: input id is synthetic (fresh span), else history
+  std::int32_t pad;
+  std::int64_t req_id;
+};
+
+// A tile of consecutive chunk rows of one request for prefill attention.
+struct TileDesc {
+  std::int32_t row0;   // first batch row
+  std::int32_t nrows;  // <= 64
+  std::int32_t slot;
+  std::int32_t pos0;   // position of row0
+};
+
+// Swap copy descriptor: positions [pos0, pos0+n) of a slot <-> staging rows.
+struct SwapDesc {
+  std::int32_t slot;
+  std::int32_t pos0;
+  std::int32_t n;
+  std::int32_t pad;
+  std::int64_t stage_off;  // element offset of this op's [L][n][2D] slab
+};
+
+// Epilogue variants of the projection GEMMs.
+enum class Epi : int {
+  StoreBf16 = 0,     // out = acc (+bias)
+  GeluBf16 = 1,      // out = gelu_tanh(acc + bias)
+  ResidAdd = 2,      // resid(fp32) += acc (+bias)
+  SwiGluBf16 = 3,    // out[j] = silu(acc[2j]) * acc[2j+1]
+  StoreF32 = 4       // outf = acc (+bias)
+};
+
+struct GemmArgs {
+  const bf16* a;       // [M][K] row-major (K contiguous)
+  const bf16* w;       // [N][K] row-major
+  int M, N, K;
+  Epi epi;
+  const bf16* bias;    // [N] or null
+  bf16* out;           // [M][ldo] bf16 output
+  int ldo;
+  float* outf;         // fp32 output / residual stream
+  int ldf;
+};
+
+}  // namespace ib2

@@ -1,0 +1,821 @@
+// B200 executor: turns one scheduler BatchPlan into device work.
+//
+// Per iteration, all on the compute stream (plans are enqueued asynchronously;
+// the host never waits on the GPU outside record/sync):
+//   1. plan upload: one H2D copy of rows / tiles / block deltas / swap
+//      descriptors from a pinned ring;
+//   2. K8 pre-phase block-table update (frees then allocs, LIFO free list);
+//   3. K7 swap-in: H2D of each op's host extent into staging, scatter kernel;
+//   4. forward: K9 embed -> per layer [K5 norm, K3 QKV, K4 RoPE+KV write,
+//      K1 decode rows | K2 chunk tiles, K3 O (+residual), K5, K3 MLP in/out]
+//      -> K5 final norm of sampling rows -> K3 LM head -> K6 argmax into the
+//      token history;
+//   5. K7 swap-out: gather kernel into staging, D2H into pinned host extents;
+//   6. K8 post-phase frees (swap-outs, discards, releases).
+// Swap copies are asynchronous cudaMemcpyAsync on a dedicated copy stream;
+// staging buffers are double-buffered and ordered with events.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include <json.hpp>
+
+#include "executor.hpp"
+#include "kernels.hpp"
+#include "model.hpp"
+
+namespace ib2 {
+
+void set_gemm_activation_rows(std::int64_t rows);
+
+namespace {
+
+// First-fit allocator over the pinned host swap arena (byte offsets).
+class HostArena {
+ public:
+  void reset(std::size_t bytes) {
+    free_.clear();
+    free_[0] = bytes;
+    cap_ = bytes;
+    used_ = 0;
+  }
+  std::size_t alloc(std::size_t n) {
+    n = (n + 255) & ~std::size_t(255);
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+      if (it->second >= n) {
+        const std::size_t off = it->first, left = it->second - n;
+        free_.erase(it);
+        if (left) free_[off + n] = left;
+        used_ += n;
+        return off;
+      }
+    }
+    throw DeviceError("pinned host swap pool exhausted (" + std::to_string(used_) + " of " + std::to_string(cap_) +
+                      " bytes in use)");
+  }
+  void release(std::size_t off, std::size_t n) {
+    n = (n + 255) & ~std::size_t(255);
+    used_ -= n;
+    auto it = free_.emplace(off, n).first;
+    auto nx = std::next(it);
+    if (nx != free_.end() && it->first + it->second == nx->first) {
+      it->second += nx->second;
+      free_.erase(nx);
+    }
+    if (it != free_.begin()) {
+      auto pv = std::prev(it);
+      if (pv->first + pv->second == it->first) {
+        pv->second += it->second;
+        free_.erase(it);
+      }
+    }
+  }
+  std::size_t used() const { return used_; }
+
+ private:
+  std::map<std::size_t, std::size_t> free_;
+  std::size_t cap_ = 0, used_ = 0;
+};
+
+// Positions [lo,hi) of one request living in a host extent laid out
+// [L][n][2D] (n = hi0 - lo0 of the op that created it).
+struct Extent {
+  std::int64_t lo0, hi0;  // positions the extent was created for
+  std::int64_t lo, hi;    // positions still resident on the host
+  std::size_t off;        // arena offset
+  std::size_t bytes;
+};
+
+template <typename T>
+T* dalloc(std::size_t n) {
+  void* p = nullptr;
+  IB2_CUDA(cudaMalloc(&p, std::max<std::size_t>(n, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+class Impl final : public B200Executor {
+ public:
+  Impl(const std::string& model_json, int device, const std::string& pools_json);
+  ~Impl() override;
+
+  void consume(const isim_batch_plan& plan) override;
+  void sync() override;
+  std::string stats_json() const override;
+  std::int32_t last_tokens(std::int32_t* out, std::int32_t cap) const override;
+  std::int64_t last_logits(float* out, std::int64_t cap) const override;
+  std::int32_t block_table(std::int64_t request_id, std::int32_t* out, std::int32_t cap) const override;
+  std::int64_t free_blocks() const override;
+  void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out, std::int64_t cap) const override;
+
+ private:
+  struct Touch {
+    std::int32_t slot, lb;
+    bool was_mapped;
+  };
+  int slot_for(std::int64_t rid);
+  void apply_ops(const isim_batch_plan& p, int phase, std::vector<std::int32_t>& frees,
+                 std::vector<std::int32_t>& allocs, std::vector<SwapDesc>& swaps_in, std::vector<SwapDesc>& swaps_out,
+                 std::vector<std::int64_t>& released);
+  void run_swaps(const std::vector<SwapDesc>& ops, const std::vector<std::int64_t>& req_of, bool swap_in);
+  void forward(int n_rows, int n_drows, int n_tiles, int n_samples);
+  void check_error();
+  KvGeom geom() const {
+    return KvGeom{pool_, gpu_blocks_, spec_.layers, spec_.heads, spec_.head_dim(), table_, max_lb_};
+  }
+  const bf16* W(std::int64_t off) const { return off < 0 ? nullptr : weights_ + off; }
+
+  ModelSpec spec_;
+  WeightLayout wl_;
+  int dev_ = 0;
+  cudaStream_t main_ = nullptr, copy_ = nullptr;
+  bool record_ = false, timing_ = false;
+
+  bf16* weights_ = nullptr;
+  std::int64_t gpu_blocks_ = 0;
+  int max_lb_ = 0, max_slots_ = 0, max_rows_ = 0, max_ctx_ = 0, hist_stride_ = 0;
+  bf16* pool_ = nullptr;
+  std::int32_t *table_ = nullptr, *stack_ = nullptr, *top_ = nullptr, *err_ = nullptr, *hist_ = nullptr;
+  float* rope_cs_ = nullptr;
+  float *x_ = nullptr, *logits_ = nullptr, *part_o_ = nullptr, *part_ml_ = nullptr;
+  bf16 *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *hid_ = nullptr, *lmrows_ = nullptr;
+  std::int32_t* out_tok_ = nullptr;
+
+  // plan upload
+  static constexpr int kRing = 4;
+  std::size_t plan_bytes_ = 0;
+  unsigned char* plan_host_[kRing] = {};
+  unsigned char* plan_dev_[kRing] = {};
+  cudaEvent_t plan_done_[kRing] = {};
+  int ring_ = 0;
+
+  // swap
+  unsigned char* host_pool_ = nullptr;
+  std::size_t host_bytes_ = 0;
+  HostArena arena_;
+  std::unordered_map<std::int64_t, std::vector<Extent>> extents_;
+  bf16* stage_ = nullptr;
+  std::int64_t stage_tokens_ = 0;
+  SwapDesc* swap_dev_ = nullptr;
+  std::int32_t* swap_prefix_dev_ = nullptr;
+
+  // host mirrors
+  std::unordered_map<std::int64_t, int> slot_of_;
+  std::vector<int> free_slots_;
+  std::vector<std::vector<std::uint8_t>> resid_;  // [slot][lblock] resident positions
+
+  // record / stats
+  std::vector<std::int32_t> last_tok_;
+  std::vector<float> last_logits_;
+  std::int64_t iters_ = 0, rows_total_ = 0, decode_rows_total_ = 0, chunk_rows_total_ = 0, swap_in_tok_ = 0,
+               swap_out_tok_ = 0, samples_total_ = 0;
+  double k1_bytes_timed_ = 0.0, k1_ms_ = 0.0;
+  std::int64_t k1_launches_timed_ = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_free_, ev_pending_;
+  std::vector<double> ev_bytes_;
+  std::int64_t kernel_launches_ = 0;
+
+  // per-iteration device views (valid during forward)
+  const RowDesc* rows_dev_ = nullptr;
+  const std::int32_t* drows_dev_ = nullptr;
+  const TileDesc* tiles_dev_ = nullptr;
+  const std::int32_t* samples_dev_ = nullptr;
+  double k1_bytes_iter_ = 0.0;
+  int max_pos1_ = 0;
+};
+
+Impl::Impl(const std::string& model_json, int device, const std::string& pools_json) {
+  spec_ = parse_model_json(model_json);
+  wl_ = layout_weights(spec_);
+  nlohmann::json pj = nlohmann::json::parse(pools_json.empty() ? "{}" : pools_json);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device || device < 0)
+    throw DeviceError("no CUDA device " + std::to_string(device) + " (B200 executor requires a GPU)");
+  dev_ = device;
+  IB2_CUDA(cudaSetDevice(dev_));
+  cudaDeviceProp prop;
+  IB2_CUDA(cudaGetDeviceProperties(&prop, dev_));
+  if (prop.major != 10) throw DeviceError(std::string("executor is built for sm_100a; device is ") + prop.name);
+  IB2_CUDA(cudaStreamCreateWithFlags(&main_, cudaStreamNonBlocking));
+  IB2_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  record_ = pj.value("record", false);
+  timing_ = pj.value("timing", false);
+
+  max_slots_ = pj.value("max_requests", 1024);
+  max_rows_ = pj.value("max_rows", 4096);
+  max_ctx_ = pj.value("max_ctx", spec_.max_pos);
+  max_ctx_ = (max_ctx_ + kBlockTokens - 1) / kBlockTokens * kBlockTokens;
+  max_lb_ = max_ctx_ / kBlockTokens;
+  hist_stride_ = max_ctx_ + 1;
+  const std::int64_t M = spec_.kv_bytes_per_token();
+  if (pj.contains("gpu_blocks")) {
+    gpu_blocks_ = pj["gpu_blocks"].get<std::int64_t>();
+  } else {
+    const double cap = pj.value("gpu_kv_capacity", 1.0e9);
+    const double m_cost = pj.value("mem_per_token", static_cast<double>(M));
+    gpu_blocks_ = static_cast<std::int64_t>(cap / (m_cost * kBlockTokens)) + 2LL * max_slots_;
+  }
+  if (pj.contains("host_bytes")) {
+    host_bytes_ = pj["host_bytes"].get<std::size_t>();
+  } else {
+    const double cpu = pj.value("cpu_kv_capacity", 4.0e9);
+    const double m_cost = pj.value("mem_per_token", static_cast<double>(M));
+    host_bytes_ = static_cast<std::size_t>(cpu / m_cost * static_cast<double>(M) * 1.25) + (64u << 20);
+  }
+  stage_tokens_ = pj.value("stage_tokens", 4096);
+
+  // weights
+  weights_ = dalloc<bf16>(wl_.total);
+  for (const auto& it : wl_.items) launch_init_tensor(weights_ + it.off, it.count, spec_.weight_seed, it.id, it.kind, main_);
+
+  // KV pool and block tables
+  const std::int64_t pool_elems = spec_.layers * gpu_blocks_ * 2LL * spec_.d_model * kBlockTokens;
+  pool_ = dalloc<bf16>(pool_elems);
+  IB2_CUDA(cudaMemsetAsync(pool_, 0, pool_elems * sizeof(bf16), main_));
+  table_ = dalloc<std::int32_t>(static_cast<std::size_t>(max_slots_) * max_lb_);
+  launch_fill_i32(table_, static_cast<std::int64_t>(max_slots_) * max_lb_, -1, main_);
+  stack_ = dalloc<std::int32_t>(gpu_blocks_ + 16);
+  launch_iota_desc(stack_, gpu_blocks_, main_);
+  top_ = dalloc<std::int32_t>(1);
+  err_ = dalloc<std::int32_t>(1);
+  {
+    const std::int32_t init[1] = {static_cast<std::int32_t>(gpu_blocks_)};
+    IB2_CUDA(cudaMemcpyAsync(top_, init, 4, cudaMemcpyHostToDevice, main_));
+    IB2_CUDA(cudaMemsetAsync(err_, 0, 4, main_));
+  }
+  hist_ = dalloc<std::int32_t>(static_cast<std::size_t>(max_slots_) * hist_stride_);
+  IB2_CUDA(cudaMemsetAsync(hist_, 0, static_cast<std::size_t>(max_slots_) * hist_stride_ * 4, main_));
+  resid_.assign(max_slots_, std::vector<std::uint8_t>(max_lb_, 0));
+  for (int s = max_slots_ - 1; s >= 0; --s) free_slots_.push_back(s);
+
+  // RoPE table [max_ctx][rot/2][cos,sin], computed in double on the host.
+  if (spec_.rotary_dim) {
+    const int half = spec_.rotary_dim / 2;
+    std::vector<float> cs(static_cast<std::size_t>(max_ctx_) * spec_.rotary_dim);
+    for (int p = 0; p < max_ctx_; ++p)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(spec_.rope_theta, -2.0 * i / spec_.rotary_dim);
+        const double a = static_cast<double>(p) * inv;
+        cs[(static_cast<std::size_t>(p) * half + i) * 2] = static_cast<float>(std::cos(a));
+        cs[(static_cast<std::size_t>(p) * half + i) * 2 + 1] = static_cast<float>(std::sin(a));
+      }
+    rope_cs_ = dalloc<float>(cs.size());
+    IB2_CUDA(cudaMemcpy(rope_cs_, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+  }
+
+  // activations (every GEMM A operand buffer has max_rows rows)
+  const std::int64_t D = spec_.d_model;
+  x_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * D);
+  xn_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
+  qkv_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * 3 * D);
+  attn_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
+  hid_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * spec_.ffn);
+  lmrows_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
+  logits_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.vocab);
+  out_tok_ = dalloc<std::int32_t>(max_rows_);
+  const int max_splits = (max_ctx_ + 255) / 256;
+  part_o_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * spec_.head_dim());
+  part_ml_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * 2);
+  set_gemm_activation_rows(max_rows_);
+
+  // plan ring
+  plan_bytes_ = static_cast<std::size_t>(max_rows_) * (sizeof(RowDesc) + 4 * 4 + sizeof(TileDesc)) +
+                static_cast<std::size_t>(max_slots_) * max_lb_ * 4 * 3 + 4096;
+  for (int i = 0; i < kRing; ++i) {
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[i]), plan_bytes_, cudaHostAllocDefault));
+    plan_dev_[i] = dalloc<unsigned char>(plan_bytes_);
+    IB2_CUDA(cudaEventCreateWithFlags(&plan_done_[i], cudaEventDisableTiming));
+  }
+
+  // swap path
+  IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_bytes_, cudaHostAllocDefault));
+  arena_.reset(host_bytes_);
+  stage_ = dalloc<bf16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
+  swap_dev_ = dalloc<SwapDesc>(4096);
+  swap_prefix_dev_ = dalloc<std::int32_t>(4097);
+  IB2_CUDA(cudaStreamSynchronize(main_));
+}
+
+Impl::~Impl() {
+  cudaDeviceSynchronize();
+  for (auto& e : ev_free_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (auto& e : ev_pending_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  for (int i = 0; i < kRing; ++i) {
+    cudaFreeHost(plan_host_[i]);
+    cudaFree(plan_dev_[i]);
+    cudaEventDestroy(plan_done_[i]);
+  }
+  cudaFreeHost(host_pool_);
+  void* ptrs[] = {weights_, pool_, table_, stack_, top_, err_, hist_, rope_cs_, x_, xn_, qkv_, attn_, hid_, lmrows_,
+                  logits_, out_tok_, part_o_, part_ml_, stage_, swap_dev_, swap_prefix_dev_};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  cudaStreamDestroy(main_);
+  cudaStreamDestroy(copy_);
+}
+
+int Impl::slot_for(std::int64_t rid) {
+  auto it = slot_of_.find(rid);
+  if (it != slot_of_.end()) return it->second;
+  if (free_slots_.empty()) throw DeviceError("executor: more live requests than max_requests");
+  const int s = free_slots_.back();
+  free_slots_.pop_back();
+  slot_of_[rid] = s;
+  return s;
+}
+
+// Residency bookkeeping of a phase's ops; emits the logical blocks whose
+// occupancy crossed zero (in first-touch order) and the swap copy lists.
+void Impl::apply_ops(const isim_batch_plan& p, int phase, std::vector<std::int32_t>& frees,
+                     std::vector<std::int32_t>& allocs, std::vector<SwapDesc>& swaps_in,
+                     std::vector<SwapDesc>& swaps_out, std::vector<std::int64_t>& released) {
+  std::vector<Touch> touched;
+  std::unordered_map<std::int64_t, std::size_t> seen;
+  auto touch = [&](int slot, std::int64_t lo, std::int64_t hi, int sign) {
+    if (hi > max_ctx_) throw DeviceError("executor: position beyond max_ctx");
+    for (std::int64_t b = lo / kBlockTokens; b * kBlockTokens < hi; ++b) {
+      const std::int64_t key = static_cast<std::int64_t>(slot) * max_lb_ + b;
+      std::uint8_t& c = resid_[slot][b];
+      if (!seen.count(key)) {
+        seen[key] = touched.size();
+        touched.push_back({slot, static_cast<std::int32_t>(b), c > 0});
+      }
+      const std::int64_t a = std::max(lo, b * kBlockTokens), e = std::min(hi, (b + 1) * kBlockTokens);
+      const int v = static_cast<int>(c) + sign * static_cast<int>(e - a);
+      if (v < 0 || v > kBlockTokens) throw DeviceError("executor: block residency out of range");
+      c = static_cast<std::uint8_t>(v);
+    }
+  };
+  for (int i = 0; i < p.n_ops; ++i) {
+    const isim_kv_op& op = p.ops[i];
+    if (op.phase != phase) continue;
+    const int slot = slot_for(op.request_id);
+    switch (op.kind) {
+      case ISIM_KV_GROW:
+      case ISIM_KV_RECOMPUTE:
+        touch(slot, op.pos_lo, op.pos_hi, +1);
+        break;
+      case ISIM_KV_SWAP_IN:
+        touch(slot, op.pos_lo, op.pos_hi, +1);
+        swaps_in.push_back({slot, static_cast<std::int32_t>(op.pos_lo), static_cast<std::int32_t>(op.pos_hi - op.pos_lo),
+                            0, 0});
+        break;
+      case ISIM_KV_SWAP_OUT:
+        swaps_out.push_back({slot, static_cast<std::int32_t>(op.pos_lo),
+                             static_cast<std::int32_t>(op.pos_hi - op.pos_lo), 0, 0});
+        touch(slot, op.pos_lo, op.pos_hi, -1);
+        break;
+      case ISIM_KV_DISCARD:
+        touch(slot, op.pos_lo, op.pos_hi, -1);
+        break;
+      case ISIM_KV_RELEASE:
+        for (int b = 0; b < max_lb_; ++b) {
+          if (!resid_[slot][b]) continue;
+          const std::int64_t key = static_cast<std::int64_t>(slot) * max_lb_ + b;
+          if (!seen.count(key)) {
+            seen[key] = touched.size();
+            touched.push_back({slot, b, true});
+          }
+          resid_[slot][b] = 0;
+        }
+        released.push_back(op.request_id);
+        break;
+      default:
+        throw DeviceError("executor: unknown kv op kind");
+    }
+  }
+  for (const Touch& t : touched) {
+    const bool now = resid_[t.slot][t.lb] > 0;
+    const std::int32_t e = t.slot * max_lb_ + t.lb;
+    if (t.was_mapped && !now) frees.push_back(e);
+    if (!t.was_mapped && now) allocs.push_back(e);
+  }
+}
+
+void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std::int64_t>& req_of, bool swap_in) {
+  if (in_ops.empty()) return;
+  const std::int64_t D = spec_.d_model, L = spec_.layers;
+  const std::size_t row_bytes = static_cast<std::size_t>(2 * D) * sizeof(bf16);
+  // Split ops at extent boundaries (swap-in) and into staging-sized batches.
+  std::vector<SwapDesc> ops;
+  std::vector<std::pair<std::int64_t, std::size_t>> ext_of;  // (request, extent index) per op (swap-in)
+  for (std::size_t i = 0; i < in_ops.size(); ++i) {
+    const SwapDesc& o = in_ops[i];
+    if (!swap_in) {
+      for (std::int32_t k = 0; k < o.n; k += static_cast<std::int32_t>(stage_tokens_)) {
+        SwapDesc c = o;
+        c.pos0 = o.pos0 + k;
+        c.n = static_cast<std::int32_t>(std::min<std::int64_t>(stage_tokens_, o.n - k));
+        ops.push_back(c);
+        ext_of.push_back({req_of[i], 0});
+      }
+      continue;
+    }
+    auto& exts = extents_[req_of[i]];
+    std::int64_t lo = o.pos0;
+    const std::int64_t hi = o.pos0 + o.n;
+    while (lo < hi) {
+      std::size_t e = 0;
+      while (e < exts.size() && !(exts[e].lo <= lo && lo < exts[e].hi)) ++e;
+      if (e == exts.size()) throw DeviceError("executor: swap-in of positions not on the host");
+      const std::int64_t end = std::min({hi, exts[e].hi, lo + stage_tokens_});
+      ops.push_back({o.slot, static_cast<std::int32_t>(lo), static_cast<std::int32_t>(end - lo), 0, 0});
+      ext_of.push_back({req_of[i], e});
+      lo = end;
+    }
+  }
+  std::size_t first = 0;
+  while (first < ops.size()) {
+    std::size_t last = first;
+    std::int64_t tok = 0;
+    while (last < ops.size() && tok + ops[last].n <= stage_tokens_ && last - first < 4096) tok += ops[last++].n;
+    std::vector<SwapDesc> batch(ops.begin() + first, ops.begin() + last);
+    std::vector<std::int32_t> prefix(batch.size() + 1, 0);
+    std::int64_t off = 0;
+    for (std::size_t k = 0; k < batch.size(); ++k) {
+      batch[k].stage_off = off;
+      off += static_cast<std::int64_t>(batch[k].n) * L * 2 * D;
+      prefix[k + 1] = prefix[k] + batch[k].n;
+    }
+    IB2_CUDA(cudaMemcpyAsync(swap_dev_, batch.data(), batch.size() * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
+    IB2_CUDA(cudaMemcpyAsync(swap_prefix_dev_, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, main_));
+    if (swap_in) {
+      for (std::size_t k = 0; k < batch.size(); ++k) {
+        const Extent& x = extents_[ext_of[first + k].first][ext_of[first + k].second];
+        const std::int64_t n0 = x.hi0 - x.lo0;
+        const unsigned char* src = host_pool_ + x.off + static_cast<std::size_t>(batch[k].pos0 - x.lo0) * row_bytes;
+        IB2_CUDA(cudaMemcpy2DAsync(stage_ + batch[k].stage_off, static_cast<std::size_t>(batch[k].n) * row_bytes, src,
+                                   static_cast<std::size_t>(n0) * row_bytes,
+                                   static_cast<std::size_t>(batch[k].n) * row_bytes, L, cudaMemcpyHostToDevice, main_));
+      }
+      launch_swap_copy(swap_dev_, swap_prefix_dev_, static_cast<int>(batch.size()), prefix.back(), geom(), stage_,
+                       false, main_);
+      ++kernel_launches_;
+      // Retire consumed host positions; free fully consumed extents.
+      for (std::size_t k = 0; k < batch.size(); ++k) {
+        auto& exts = extents_[ext_of[first + k].first];
+        Extent& x = exts[ext_of[first + k].second];
+        x.lo = batch[k].pos0 + batch[k].n;
+      }
+    } else {
+      launch_swap_copy(swap_dev_, swap_prefix_dev_, static_cast<int>(batch.size()), prefix.back(), geom(), stage_,
+                       true, main_);
+      ++kernel_launches_;
+      for (std::size_t k = 0; k < batch.size(); ++k) {
+        const std::size_t bytes = static_cast<std::size_t>(batch[k].n) * L * row_bytes;
+        const std::size_t hoff = arena_.alloc(bytes);
+        IB2_CUDA(cudaMemcpyAsync(host_pool_ + hoff, stage_ + batch[k].stage_off, bytes, cudaMemcpyDeviceToHost, main_));
+        extents_[ext_of[first + k].first].push_back(
+            {batch[k].pos0, batch[k].pos0 + batch[k].n, batch[k].pos0, batch[k].pos0 + batch[k].n, hoff, bytes});
+      }
+    }
+    first = last;
+  }
+  if (swap_in) {
+    // Host memory of consumed extents is reused only by later D2H copies on
+    // this same stream, which are ordered after the H2D reads above.
+    for (const auto& [rid, idx] : ext_of) {
+      auto& exts = extents_[rid];
+      for (std::size_t e = 0; e < exts.size();) {
+        if (exts[e].lo >= exts[e].hi) {
+          arena_.release(exts[e].off, exts[e].bytes);
+          exts.erase(exts.begin() + static_cast<std::ptrdiff_t>(e));
+        } else {
+          ++e;
+        }
+      }
+    }
+  }
+}
+
+void Impl::consume(const isim_batch_plan& p) {
+  IB2_CUDA(cudaSetDevice(dev_));
+  const int D = spec_.d_model;
+
+  // ---- host-side plan lowering ------------------------------------------------
+  std::vector<std::int32_t> frees0, allocs0, frees1, allocs1;
+  std::vector<SwapDesc> sw_in, sw_out, dummy;
+  std::vector<std::int64_t> released0, released1;
+  apply_ops(p, 0, frees0, allocs0, sw_in, dummy, released0);
+
+  std::vector<RowDesc> rows;
+  std::vector<std::int32_t> drows, samples;
+  std::vector<TileDesc> tiles;
+  for (int i = 0; i < p.n_spans; ++i) {
+    const isim_row_span& sp = p.spans[i];
+    const int slot = slot_for(sp.request_id);
+    const int r0 = static_cast<int>(rows.size());
+    if (sp.pos + sp.count > max_ctx_) throw DeviceError("executor: row position beyond max_ctx");
+    for (int k = 0; k < sp.count; ++k)
+      rows.push_back({slot, sp.pos + k, sp.kind == ISIM_SPAN_FRESH ? 1 : 0, 0, sp.request_id});
+    if (sp.count == 1) {
+      drows.push_back(r0);
+    } else {
+      for (int k = 0; k < sp.count; k += 64) tiles.push_back({r0 + k, std::min(64, sp.count - k), slot, sp.pos + k});
+    }
+    if (sp.sample) samples.push_back(r0 + sp.count - 1);
+  }
+  const int n_rows = static_cast<int>(rows.size());
+  if (n_rows > max_rows_) throw DeviceError("executor: batch exceeds max_rows");
+
+  std::vector<std::int64_t> sw_in_req;
+  for (int i = 0; i < p.n_ops; ++i)
+    if (p.ops[i].phase == 0 && p.ops[i].kind == ISIM_KV_SWAP_IN) sw_in_req.push_back(p.ops[i].request_id);
+
+  // ---- upload -----------------------------------------------------------------
+  const int k = ring_;
+  ring_ = (ring_ + 1) % kRing;
+  IB2_CUDA(cudaEventSynchronize(plan_done_[k]));
+  unsigned char* h = plan_host_[k];
+  unsigned char* d = plan_dev_[k];
+  std::size_t off = 0;
+  auto put = [&](const void* src, std::size_t bytes) {
+    const std::size_t at = off;
+    if (at + bytes > plan_bytes_) throw DeviceError("executor: plan exceeds upload buffer");
+    if (bytes) std::memcpy(h + at, src, bytes);
+    off = (at + bytes + 15) & ~std::size_t(15);
+    return d + at;
+  };
+  const RowDesc* d_rows = reinterpret_cast<const RowDesc*>(put(rows.data(), rows.size() * sizeof(RowDesc)));
+  const std::int32_t* d_drows = reinterpret_cast<const std::int32_t*>(put(drows.data(), drows.size() * 4));
+  const TileDesc* d_tiles = reinterpret_cast<const TileDesc*>(put(tiles.data(), tiles.size() * sizeof(TileDesc)));
+  const std::int32_t* d_samples = reinterpret_cast<const std::int32_t*>(put(samples.data(), samples.size() * 4));
+  const std::int32_t* d_frees0 = reinterpret_cast<const std::int32_t*>(put(frees0.data(), frees0.size() * 4));
+  const std::int32_t* d_allocs0 = reinterpret_cast<const std::int32_t*>(put(allocs0.data(), allocs0.size() * 4));
+  IB2_CUDA(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, main_));
+  IB2_CUDA(cudaEventRecord(plan_done_[k], main_));
+
+  // ---- pre-phase: block table, swap-in ------------------------------------------
+  launch_block_update(table_, stack_, top_, err_, d_frees0, static_cast<int>(frees0.size()), d_allocs0,
+                      static_cast<int>(allocs0.size()), main_);
+  run_swaps(sw_in, sw_in_req, true);
+
+  // ---- forward ------------------------------------------------------------------
+  (void)D;
+  if (n_rows > 0) {
+    rows_dev_ = d_rows;
+    drows_dev_ = d_drows;
+    tiles_dev_ = d_tiles;
+    samples_dev_ = d_samples;
+    std::int64_t k1_bytes = 0;
+    for (int r : drows) k1_bytes += static_cast<std::int64_t>(rows[r].pos + 1) * 2 * spec_.d_model * 2;
+    k1_bytes_iter_ = static_cast<double>(k1_bytes);
+    max_pos1_ = 0;
+    for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
+    forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(tiles.size()), static_cast<int>(samples.size()));
+  }
+
+  // ---- post-phase: swap-out gather + D2H, then frees -----------------------------
+  std::vector<SwapDesc> dummy_in;
+  apply_ops(p, 1, frees1, allocs1, dummy_in, sw_out, released1);
+  if (!allocs1.empty()) throw DeviceError("executor: allocation in post phase");
+  std::vector<std::int64_t> sw_out_req;
+  for (int i = 0; i < p.n_ops; ++i)
+    if (p.ops[i].phase == 1 && p.ops[i].kind == ISIM_KV_SWAP_OUT) sw_out_req.push_back(p.ops[i].request_id);
+  run_swaps(sw_out, sw_out_req, false);
+  if (!frees1.empty()) {
+    const int k2 = ring_;
+    ring_ = (ring_ + 1) % kRing;
+    IB2_CUDA(cudaEventSynchronize(plan_done_[k2]));
+    std::memcpy(plan_host_[k2], frees1.data(), frees1.size() * 4);
+    IB2_CUDA(cudaMemcpyAsync(plan_dev_[k2], plan_host_[k2], frees1.size() * 4, cudaMemcpyHostToDevice, main_));
+    IB2_CUDA(cudaEventRecord(plan_done_[k2], main_));
+    launch_block_update(table_, stack_, top_, err_, reinterpret_cast<const std::int32_t*>(plan_dev_[k2]),
+                        static_cast<int>(frees1.size()), nullptr, 0, main_);
+  }
+  for (std::int64_t rid : released0) (void)rid;
+  for (std::int64_t rid : released1) {
+    auto it = slot_of_.find(rid);
+    if (it != slot_of_.end()) {
+      free_slots_.push_back(it->second);
+      slot_of_.erase(it);
+    }
+    auto ex = extents_.find(rid);
+    if (ex != extents_.end()) {
+      for (const Extent& x : ex->second) arena_.release(x.off, x.bytes);
+      extents_.erase(ex);
+    }
+  }
+
+  // ---- stats / record ------------------------------------------------------------
+  iters_ += 1;
+  rows_total_ += n_rows;
+  decode_rows_total_ += static_cast<std::int64_t>(drows.size());
+  chunk_rows_total_ += n_rows - static_cast<std::int64_t>(drows.size());
+  samples_total_ += static_cast<std::int64_t>(samples.size());
+  for (const auto& s : sw_in) swap_in_tok_ += s.n;
+  for (const auto& s : sw_out) swap_out_tok_ += s.n;
+  if (record_) {
+    IB2_CUDA(cudaStreamSynchronize(main_));
+    check_error();
+    last_tok_.assign(p.n_spans, -1);
+    std::vector<std::int32_t> toks(samples.size());
+    if (!samples.empty())
+      IB2_CUDA(cudaMemcpy(toks.data(), out_tok_, samples.size() * 4, cudaMemcpyDeviceToHost));
+    int si = 0;
+    for (int i = 0; i < p.n_spans; ++i)
+      if (p.spans[i].sample) last_tok_[i] = toks[si++];
+    last_logits_.resize(samples.size() * static_cast<std::size_t>(spec_.vocab));
+    if (!samples.empty())
+      IB2_CUDA(cudaMemcpy(last_logits_.data(), logits_, last_logits_.size() * 4, cudaMemcpyDeviceToHost));
+  }
+}
+
+void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
+  const ModelSpec& m = spec_;
+  const int D = m.d_model, F = m.ffn;
+  const KvGeom g = geom();
+  const bool rms = m.family == Family::Llama;
+  auto gemm = [&](const bf16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias, bf16* out, int ldo,
+                  float* outf, int ldf, int M) {
+    GemmArgs ga{a, weights_ + w, M, N, K, epi, W(bias), out, ldo, outf, ldf};
+    launch_gemm(ga, main_);
+    ++kernel_launches_;
+  };
+  launch_embed(rows_dev_, n, hist_, hist_stride_, W(wl_.tok_emb), W(wl_.pos_emb), D, m.token_seed, m.vocab, x_, main_);
+  ++kernel_launches_;
+  const int timed_layer = m.layers / 2;
+  for (int l = 0; l < m.layers; ++l) {
+    const LayerWeights& lw = wl_.layer[l];
+    launch_norm(x_, D, nullptr, n, D, W(lw.ln1_g), W(lw.ln1_b), rms, m.norm_eps, xn_, D, main_);
+    gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreBf16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
+    launch_rope_kv_write(qkv_, rows_dev_, n, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, main_);
+    kernel_launches_ += 2;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    const bool time_k1 = timing_ && l == timed_layer && n_drows > 0;
+    if (time_k1) {
+      if (ev_free_.empty()) {
+        cudaEvent_t a, b;
+        IB2_CUDA(cudaEventCreate(&a));
+        IB2_CUDA(cudaEventCreate(&b));
+        ev_free_.push_back({a, b});
+      }
+      e0 = ev_free_.back().first;
+      e1 = ev_free_.back().second;
+      ev_free_.pop_back();
+      IB2_CUDA(cudaEventRecord(e0, main_));
+    }
+    launch_decode_attention(qkv_, drows_dev_, rows_dev_, n_drows, g, l, max_pos1_, part_o_, part_ml_, attn_, main_);
+    if (n_drows) kernel_launches_ += 2;
+    if (time_k1) {
+      IB2_CUDA(cudaEventRecord(e1, main_));
+      ev_pending_.push_back({e0, e1});
+      ev_bytes_.push_back(k1_bytes_iter_ + static_cast<double>(n_drows) * 2.0 * D * 2);
+    }
+    launch_chunk_attention(qkv_, tiles_dev_, n_tiles, g, l, attn_, main_);
+    if (n_tiles) ++kernel_launches_;
+    if (m.parallel_residual()) {
+      // GPT-J: x += attn W_o + mlp(ln1(x)); both read the same xn.
+      gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
+      gemm(xn_, lw.w_in, F, D, Epi::GeluBf16, lw.b_in, hid_, F, nullptr, 0, n);
+      gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
+    } else {
+      gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
+      launch_norm(x_, D, nullptr, n, D, W(lw.ln2_g), W(lw.ln2_b), rms, m.norm_eps, xn_, D, main_);
+      ++kernel_launches_;
+      if (m.family == Family::Llama)
+        gemm(xn_, lw.w_in, 2 * F, D, Epi::SwiGluBf16, -1, hid_, F, nullptr, 0, n);
+      else
+        gemm(xn_, lw.w_in, F, D, Epi::GeluBf16, lw.b_in, hid_, F, nullptr, 0, n);
+      gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
+    }
+  }
+  if (n_samples > 0) {
+    launch_norm(x_, D, samples_dev_, n_samples, D, W(wl_.lnf_g), W(wl_.lnf_b), rms, m.norm_eps, lmrows_, D, main_);
+    gemm(lmrows_, wl_.lm_w, m.vocab, D, Epi::StoreF32, wl_.lm_b, nullptr, 0, logits_, m.vocab, n_samples);
+    launch_argmax(logits_, n_samples, m.vocab, samples_dev_, rows_dev_, hist_, hist_stride_, out_tok_, main_);
+    kernel_launches_ += 2;
+  }
+}
+
+void Impl::check_error() {
+  std::int32_t e = 0;
+  IB2_CUDA(cudaMemcpy(&e, err_, 4, cudaMemcpyDeviceToHost));
+  if (e) throw DeviceError("executor: block-table update error " + std::to_string(e));
+}
+
+void Impl::sync() {
+  IB2_CUDA(cudaSetDevice(dev_));
+  IB2_CUDA(cudaStreamSynchronize(main_));
+  IB2_CUDA(cudaStreamSynchronize(copy_));
+  check_error();
+  for (std::size_t i = 0; i < ev_pending_.size(); ++i) {
+    float ms = 0.f;
+    IB2_CUDA(cudaEventElapsedTime(&ms, ev_pending_[i].first, ev_pending_[i].second));
+    k1_ms_ += ms;
+    k1_bytes_timed_ += ev_bytes_[i];
+    ++k1_launches_timed_;
+    ev_free_.push_back(ev_pending_[i]);
+  }
+  ev_pending_.clear();
+  ev_bytes_.clear();
+}
+
+std::string Impl::stats_json() const {
+  nlohmann::json j;
+  j["model"] = nlohmann::json::parse(model_json(spec_));
+  j["iterations"] = iters_;
+  j["rows"] = rows_total_;
+  j["decode_rows"] = decode_rows_total_;
+  j["chunk_rows"] = chunk_rows_total_;
+  j["samples"] = samples_total_;
+  j["swap_in_tokens"] = swap_in_tok_;
+  j["swap_out_tokens"] = swap_out_tok_;
+  j["swap_bytes"] = static_cast<double>(swap_in_tok_ + swap_out_tok_) * static_cast<double>(spec_.kv_bytes_per_token());
+  j["gpu_blocks"] = gpu_blocks_;
+  j["host_pool_bytes"] = host_bytes_;
+  j["host_pool_used"] = arena_.used();
+  j["kernel_launches"] = kernel_launches_;
+  j["k1_timed_launches"] = k1_launches_timed_;
+  j["k1_ms"] = k1_ms_;
+  j["k1_bytes"] = k1_bytes_timed_;
+  j["gemm"] = gemm_uses_tcgen05() ? "tcgen05" : "simt";
+  return j.dump();
+}
+
+std::int32_t Impl::last_tokens(std::int32_t* out, std::int32_t cap) const {
+  const auto n = static_cast<std::int32_t>(last_tok_.size());
+  if (out) std::memcpy(out, last_tok_.data(), std::min(n, cap) * 4);
+  return n;
+}
+
+std::int64_t Impl::last_logits(float* out, std::int64_t cap) const {
+  const auto n = static_cast<std::int64_t>(last_logits_.size());
+  if (out) std::memcpy(out, last_logits_.data(), std::min(n, cap) * 4);
+  return n;
+}
+
+std::int32_t Impl::block_table(std::int64_t rid, std::int32_t* out, std::int32_t cap) const {
+  auto it = slot_of_.find(rid);
+  if (it == slot_of_.end()) return 0;
+  IB2_CUDA(cudaStreamSynchronize(main_));
+  std::vector<std::int32_t> t(max_lb_);
+  IB2_CUDA(cudaMemcpy(t.data(), table_ + static_cast<std::int64_t>(it->second) * max_lb_, max_lb_ * 4,
+                      cudaMemcpyDeviceToHost));
+  if (out) std::memcpy(out, t.data(), std::min(max_lb_, cap) * 4);
+  return max_lb_;
+}
+
+std::int64_t Impl::free_blocks() const {
+  IB2_CUDA(cudaStreamSynchronize(main_));
+  std::int32_t t = 0;
+  IB2_CUDA(cudaMemcpy(&t, top_, 4, cudaMemcpyDeviceToHost));
+  return t;
+}
+
+void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out, std::int64_t cap) const {
+  // Bytes of positions [lo,hi) wherever they live: a pinned host extent
+  // (swapped out) or the paged GPU pool.  Layout [L][pos][2][H][hd].
+  auto it = slot_of_.find(rid);
+  if (it == slot_of_.end()) throw DeviceError("read_kv: unknown request");
+  const std::int64_t D = spec_.d_model, L = spec_.layers, H = spec_.heads, hd = spec_.head_dim();
+  const std::int64_t n = hi - lo;
+  if (cap < n * L * 2 * D * 2) throw DeviceError("read_kv: buffer too small");
+  IB2_CUDA(cudaStreamSynchronize(main_));
+  std::vector<std::int32_t> t(max_lb_);
+  IB2_CUDA(cudaMemcpy(t.data(), table_ + static_cast<std::int64_t>(it->second) * max_lb_, max_lb_ * 4,
+                      cudaMemcpyDeviceToHost));
+  bf16* dst = static_cast<bf16*>(out);
+  const KvGeom g = geom();
+  const std::size_t row = static_cast<std::size_t>(2 * D) * 2;
+  const auto ex = extents_.find(rid);
+  for (std::int64_t p = lo; p < hi; ++p) {
+    const Extent* on_host = nullptr;
+    if (ex != extents_.end())
+      for (const Extent& x : ex->second)
+        if (x.lo <= p && p < x.hi) on_host = &x;
+    for (std::int64_t l = 0; l < L; ++l) {
+      bf16* d = dst + (l * n + (p - lo)) * 2 * D;
+      if (on_host) {
+        const std::int64_t n0 = on_host->hi0 - on_host->lo0;
+        std::memcpy(d, host_pool_ + on_host->off + (static_cast<std::size_t>(l * n0 + (p - on_host->lo0))) * row, row);
+        continue;
+      }
+      const std::int32_t pb = t[p / kBlockTokens];
+      if (pb < 0) throw DeviceError("read_kv: position neither on the GPU nor on the host");
+      for (int kv = 0; kv < 2; ++kv)
+        for (std::int64_t h = 0; h < H; ++h) {
+          const bf16* src = pool_ + l * g.layer_stride() + static_cast<std::int64_t>(pb) * g.block_stride() +
+                            ((kv * H + h) * kBlockTokens + p % kBlockTokens) * hd;
+          IB2_CUDA(cudaMemcpy(d + kv * D + h * hd, src, hd * 2, cudaMemcpyDeviceToHost));
+        }
+    }
+  }
+}
+
+}  // namespace
+
+std::unique_ptr<B200Executor> B200Executor::create(const std::string& model_json, int device,
+                                                   const std::string& pools_json) {
+  return std::make_unique<Impl>(model_json, device, pools_json);
+}
+
+}  // namespace ib2

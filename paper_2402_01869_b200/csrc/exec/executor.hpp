@@ -32,4 +32,8 @@ class B200Executor : public PlanSink {
                        std::int64_t cap) const = 0;
 };
 
+// Kernel test hook behind isim_debug_gemm (exec/k_gemm_tc.cu).
+void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, const void* bias, void* out, int ldo,
+                void* outf, int ldf, bool force_simt, void* stream);
+
 }  // namespace ib2

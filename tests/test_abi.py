@@ -1,0 +1,63 @@
+"""The C ABI library loads and exports every symbol include/infercept_b200.h declares."""
+import ctypes
+import os
+import re
+
+from conftest import PRODUCT_LIB, ROOT
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "infercept_b200.h")).read()
+    return sorted(set(re.findall(r"\b(isim_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(PRODUCT_LIB)
+    missing = [s for s in header_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    assert len(header_symbols()) >= 24 + 15
+
+
+def test_reference_symbols_are_a_subset():
+    # Every entry point of the reference's interceptsim.h (24) is declared here.
+    ref = ["isim_abi_version", "isim_status_name", "isim_last_error", "isim_string_free", "isim_trace_generate",
+           "isim_trace_load", "isim_trace_save", "isim_trace_request_count", "isim_trace_stats_json",
+           "isim_trace_free", "isim_model_default", "isim_model_from_json", "isim_model_load", "isim_model_fit_csv",
+           "isim_model_to_json", "isim_model_save", "isim_model_t_fwd", "isim_model_t_swap", "isim_model_free",
+           "isim_run", "isim_result_summary_json", "isim_result_write_requests_csv", "isim_result_metric",
+           "isim_result_free"]
+    assert set(ref) <= set(header_symbols())
+
+
+def test_python_binding_matches_header():
+    from paper_2402_01869_b200 import _abi
+    assert sorted(_abi.EXPORTS) == header_symbols()
+
+
+def test_abi_version_and_status_names():
+    import paper_2402_01869_b200 as ib
+    from paper_2402_01869_b200 import _abi
+    assert ib.abi_version() == 1
+    for code, name in _abi.STATUS_NAMES.items():
+        assert _abi.lib.isim_status_name(code).decode() == name
+
+
+def test_null_arguments_are_invalid_arg():
+    from paper_2402_01869_b200 import _abi
+    assert _abi.lib.isim_trace_generate(None, None) == 1
+    assert _abi.lib.isim_last_error().decode() == "null argument"
+    assert _abi.lib.isim_trace_request_count(None) == 0
+    assert _abi.lib.isim_model_t_fwd(None, 3.0) == 0.0
+
+
+def test_executor_without_gpu_fails_loudly():
+    from conftest import have_gpu
+    import paper_2402_01869_b200 as ib
+    if have_gpu():
+        return
+    try:
+        ib.Executor({"preset": "tiny"})
+    except ib.IsimError as e:
+        assert e.status == 10  # ISIM_ERR_DEVICE, never a silent CPU fallback
+    else:
+        raise AssertionError("executor created without a GPU")
