@@ -165,6 +165,9 @@ isim_status isim_exec_free_blocks(const isim_exec* ex, int64_t* out);
 /* Raw KV bytes of [pos_lo,pos_hi) of one request, layer-major, for swap checks. */
 isim_status isim_exec_read_kv(const isim_exec* ex, int64_t request_id, int64_t pos_lo, int64_t pos_hi, void* out,
                               int64_t capacity);
+/* Device timing on the executor's compute stream: op 0 marks the start, op 1
+ * the stop; op 2 waits for the stop mark and writes the elapsed ms. */
+isim_status isim_exec_timer(isim_exec* ex, int32_t op, double* out_ms);
 void isim_exec_free(isim_exec* ex);
 
 /* ---- Part 2c: stepping session -------------------------------------------- */
@@ -182,8 +185,8 @@ void isim_session_free(isim_session* s);
 /* ---- Part 2d: kernel test hook ------------------------------------------- */
 
 /* K3 projection GEMM on caller device pointers: C = A[M][K] . W[N][K]^T with
- * epilogue epi (0 store bf16 (+bias), 1 gelu(acc+bias) bf16, 2 fp32 residual
- * add (+bias), 3 SwiGLU pairs -> bf16 [M][N/2], 4 store fp32 (+bias)).
+ * epilogue epi (0 store fp16 (+bias), 1 gelu(acc+bias) fp16, 2 fp32 residual
+ * add (+bias), 3 SwiGLU pairs -> fp16 [M][N/2], 4 store fp32 (+bias)).
  * force_simt=1 runs the CUDA-core kernel instead of tcgen05. stream may be 0. */
 isim_status isim_debug_gemm(const void* a, const void* w, int32_t M, int32_t N, int32_t K, int32_t epi,
                             const void* bias, void* out, int32_t ldo, void* outf, int32_t ldf, int32_t force_simt,

@@ -8,7 +8,7 @@ has no model -- its model step is the analytic CostModel::t_fwd
 (proj/include/interceptsim/cost_model.hpp:33-37, called at
 proj/src/engine.cpp:460) -- so there are no logits or token ids to pin against.
 This module restates the forward the executor runs, in float32 numpy with the
-same bf16 rounding points (GEMM inputs, q/k/v, attention output, KV cache), and
+same fp16 rounding points (GEMM inputs, q/k/v, attention output, KV cache), and
 consumes the very BatchPlans the scheduler emits.  The *scheduling* that
 produces those plans is pinned bit-exactly against the reference itself
 (oracle/_ref, see tests/test_sched_parity.py).
@@ -55,12 +55,10 @@ def synth_token(seed: int, rid: int, pos, vocab: int):
         return (mix64(base + np.asarray(pos, dtype=np.uint64)) % np.uint64(vocab)).astype(np.int64)
 
 
-def bf16(x: np.ndarray) -> np.ndarray:
-    """Round float32 to bfloat16 (nearest-even), returned as float32."""
-    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
-    r = ((u >> np.uint32(16)) & np.uint32(1)) + np.uint32(0x7FFF)
-    with np.errstate(over="ignore"):
-        return ((u + r) & np.uint32(0xFFFF0000)).view(np.float32)
+def r16(x: np.ndarray) -> np.ndarray:
+    """Round float32 to IEEE fp16 (nearest-even), returned as float32: the
+    executor's storage type for weights, activations and the KV cache."""
+    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
 
 
 PRESETS = {
@@ -73,7 +71,10 @@ PRESETS = {
 class ModelOracle:
     """Weights + forward of one model (exec/model.cpp layout_weights order)."""
 
-    def __init__(self, spec: dict):
+    def __init__(self, spec: dict, fast_random: bool = False):
+        # fast_random: plain numpy normals instead of the device hash, for the
+        # bench's CPU timing sample only (values then differ from the device).
+        self.fast_random = fast_random
         s = dict(PRESETS[spec.get("preset", "tiny")])
         s.update({k: v for k, v in spec.items() if k != "preset"})
         s.setdefault("max_pos", 4160)
@@ -127,7 +128,9 @@ class ModelOracle:
             return np.ones(count, np.float32)
         if kind == 2:
             return np.zeros(count, np.float32)
-        return bf16(synth_weight(self.s["weight_seed"], tid, count))
+        if self.fast_random:
+            return (np.random.default_rng(tid).standard_normal(count, dtype=np.float32) * np.float32(0.02))
+        return r16(synth_weight(self.s["weight_seed"], tid, count))
 
     # ---- pieces ---------------------------------------------------------------
     def norm(self, x, g, b):
@@ -142,7 +145,7 @@ class ModelOracle:
             y = d * (np.float32(1.0) / np.sqrt(var + np.float32(self.s["norm_eps"]))) * g
             if b is not None:
                 y = y + b
-        return bf16(y.astype(np.float32))
+        return r16(y.astype(np.float32))
 
     @staticmethod
     def lin(x, w, b=None):
@@ -150,7 +153,7 @@ class ModelOracle:
         return y + b if b is not None else y
 
     def rope(self, t, pos):
-        """t: [n, H, hd] bf16-valued float32; rotated in float32, re-rounded."""
+        """t: [n, H, hd] fp16-valued float32; rotated in float32, re-rounded."""
         if not self.rot:
             return t
         half = self.rot // 2
@@ -165,16 +168,16 @@ class ModelOracle:
             a, b = t[..., :half].copy(), t[..., half:self.rot].copy()
             t[..., :half] = a * c - b * s
             t[..., half:self.rot] = b * c + a * s
-        return bf16(t)
+        return r16(t)
 
 
 class ForwardOracle:
     """Replays BatchPlans (dicts from the scheduler's plan log) on the CPU."""
 
-    def __init__(self, model_spec: dict):
-        self.m = ModelOracle(model_spec)
+    def __init__(self, model_spec: dict, fast_random: bool = False):
+        self.m = ModelOracle(model_spec, fast_random)
         self.hist = {}     # rid -> int64[ctx]
-        self.kv = {}       # rid -> float32[L, cap, 2, D] (bf16 values)
+        self.kv = {}       # rid -> float32[L, cap, 2, D] (fp16 values)
 
     def _ensure(self, rid, upto):
         L, D = self.m.L, self.m.D
@@ -198,10 +201,6 @@ class ForwardOracle:
         both sides continue from identical inputs (ties stay harmless)."""
         m = self.m
         D, H, hd, V = m.D, m.H, m.hd, m.V
-        for (rid, kind, _phase, lo, hi) in plan["ops"]:
-            if kind == 5:  # release
-                self.hist.pop(rid, None)
-                self.kv.pop(rid, None)
         rows_rid, rows_pos, sample_rows, spans = [], [], [], []
         for (rid, pos, count, kind, sample) in plan["spans"]:
             self._ensure(rid, pos + count + 1)
@@ -214,6 +213,20 @@ class ForwardOracle:
             spans.append((rid, pos, count, r0))
             if sample:
                 sample_rows.append(r0 + count - 1)
+        out = self._forward(plan, rows_rid, rows_pos, sample_rows, spans, teacher_tokens)
+        for (rid, kind, phase, lo, hi) in plan["ops"]:
+            if kind == 5:  # release (phase 1: after this iteration's forward)
+                self.hist.pop(rid, None)
+                self.kv.pop(rid, None)
+        return out
+
+    def _forward_only(self, plan: dict) -> dict:
+        """Timing entry for the bench's CPU baseline (no teacher forcing)."""
+        return self.step(plan)
+
+    def _forward(self, plan, rows_rid, rows_pos, sample_rows, spans, teacher_tokens):
+        m = self.m
+        D, H, hd, V = m.D, m.H, m.hd, m.V
         n = len(rows_rid)
         if n == 0:
             return {"logits": np.zeros((0, V), np.float32), "tokens": [], "margin": []}
@@ -225,7 +238,7 @@ class ForwardOracle:
         scale = np.float32(1.0 / math.sqrt(hd))
         for li, lw in enumerate(m.layers):
             xn = m.norm(x, lw["ln1_g"], lw["ln1_b"])
-            qkv = bf16(m.lin(xn, lw["w_qkv"], lw["b_qkv"]))
+            qkv = r16(m.lin(xn, lw["w_qkv"], lw["b_qkv"]))
             q = m.rope(qkv[:, :D].reshape(n, H, hd), pos_arr)
             k = m.rope(qkv[:, D:2 * D].reshape(n, H, hd), pos_arr)
             v = qkv[:, 2 * D:].reshape(n, H, hd)
@@ -246,11 +259,11 @@ class ForwardOracle:
                 p = p / p.sum(axis=-1, keepdims=True)
                 o = np.einsum("hck,khd->chd", p, Vv).astype(np.float32)
                 attn[r0:r0 + count] = o.reshape(count, D)
-            attn = bf16(attn)
+            attn = r16(attn)
             if m.fam == "gptj":
                 x = x + m.lin(attn, lw["w_o"], lw["b_o"])
                 u = m.lin(xn, lw["w_in"], lw["b_in"])
-                u = bf16(_gelu(u))
+                u = r16(_gelu(u))
                 x = x + m.lin(u, lw["w_out"], lw["b_out"])
             else:
                 x = x + m.lin(attn, lw["w_o"], lw["b_o"])
@@ -258,9 +271,9 @@ class ForwardOracle:
                 if m.fam == "llama":
                     gu = m.lin(xn2, lw["w_in"])
                     g, u = gu[:, 0::2], gu[:, 1::2]
-                    h = bf16((g / (np.float32(1) + np.exp(-g))) * u)
+                    h = r16((g / (np.float32(1) + np.exp(-g))) * u)
                 else:
-                    h = bf16(_gelu(m.lin(xn2, lw["w_in"], lw["b_in"])))
+                    h = r16(_gelu(m.lin(xn2, lw["w_in"], lw["b_in"])))
                 x = x + m.lin(h, lw["w_out"], lw["b_out"])
         if not sample_rows:
             return {"logits": np.zeros((0, V), np.float32), "tokens": [], "margin": []}

@@ -199,6 +199,15 @@ class Executor(_Handle):
     def sync(self) -> None:
         _abi.check(_L.isim_exec_sync(self._ptr))
 
+    def mark(self, which: int) -> None:
+        """Record the start (0) / stop (1) timing mark on the compute stream."""
+        _abi.check(_L.isim_exec_timer(self._ptr, which, None))
+
+    def elapsed_ms(self) -> float:
+        v = ctypes.c_double()
+        _abi.check(_L.isim_exec_timer(self._ptr, 2, ctypes.byref(v)))
+        return v.value
+
     def stats(self) -> dict:
         s = ctypes.c_void_p()
         _abi.check(_L.isim_exec_stats_json(self._ptr, ctypes.byref(s)))

@@ -1,7 +1,7 @@
 // Device-side vocabulary shared by the executor's kernels.
 #pragma once
 
-#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -9,7 +9,7 @@
 
 namespace ib2 {
 
-using bf16 = __nv_bfloat16;
+using f16 = __half;  // activations, KV cache and weights; fp32 accumulation
 
 #define IB2_CUDA(expr)                                                                            \
   do {                                                                                            \
@@ -74,20 +74,20 @@ struct SwapDesc {
 
 // Epilogue variants of the projection GEMMs.
 enum class Epi : int {
-  StoreBf16 = 0,     // out = acc (+bias)
-  GeluBf16 = 1,      // out = gelu_tanh(acc + bias)
+  StoreF16 = 0,     // out = acc (+bias)
+  GeluF16 = 1,      // out = gelu_tanh(acc + bias)
   ResidAdd = 2,      // resid(fp32) += acc (+bias)
-  SwiGluBf16 = 3,    // out[j] = silu(acc[2j]) * acc[2j+1]
+  SwiGluF16 = 3,    // out[j] = silu(acc[2j]) * acc[2j+1]
   StoreF32 = 4       // outf = acc (+bias)
 };
 
 struct GemmArgs {
-  const bf16* a;       // [M][K] row-major (K contiguous)
-  const bf16* w;       // [N][K] row-major
+  const f16* a;       // [M][K] row-major (K contiguous)
+  const f16* w;       // [N][K] row-major
   int M, N, K;
   Epi epi;
-  const bf16* bias;    // [N] or null
-  bf16* out;           // [M][ldo] bf16 output
+  const f16* bias;    // [N] or null
+  f16* out;           // [M][ldo] f16 output
   int ldo;
   float* outf;         // fp32 output / residual stream
   int ldf;

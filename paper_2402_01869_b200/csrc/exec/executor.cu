@@ -125,22 +125,23 @@ class Impl final : public B200Executor {
   KvGeom geom() const {
     return KvGeom{pool_, gpu_blocks_, spec_.layers, spec_.heads, spec_.head_dim(), table_, max_lb_};
   }
-  const bf16* W(std::int64_t off) const { return off < 0 ? nullptr : weights_ + off; }
+  const f16* W(std::int64_t off) const { return off < 0 ? nullptr : weights_ + off; }
 
   ModelSpec spec_;
   WeightLayout wl_;
   int dev_ = 0;
   cudaStream_t main_ = nullptr, copy_ = nullptr;
   bool record_ = false, timing_ = false;
+  bool force_row_attention_ = false;  // diagnostics: every row through K1
 
-  bf16* weights_ = nullptr;
+  f16* weights_ = nullptr;
   std::int64_t gpu_blocks_ = 0;
   int max_lb_ = 0, max_slots_ = 0, max_rows_ = 0, max_ctx_ = 0, hist_stride_ = 0;
-  bf16* pool_ = nullptr;
+  f16* pool_ = nullptr;
   std::int32_t *table_ = nullptr, *stack_ = nullptr, *top_ = nullptr, *err_ = nullptr, *hist_ = nullptr;
   float* rope_cs_ = nullptr;
   float *x_ = nullptr, *logits_ = nullptr, *part_o_ = nullptr, *part_ml_ = nullptr;
-  bf16 *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *hid_ = nullptr, *lmrows_ = nullptr;
+  f16 *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *hid_ = nullptr, *lmrows_ = nullptr;
   std::int32_t* out_tok_ = nullptr;
 
   // plan upload
@@ -156,10 +157,44 @@ class Impl final : public B200Executor {
   std::size_t host_bytes_ = 0;
   HostArena arena_;
   std::unordered_map<std::int64_t, std::vector<Extent>> extents_;
-  bf16* stage_ = nullptr;
+  // Double-buffered swap staging.  Swap-outs: gather kernel (compute stream)
+  // -> D2H on the copy stream, overlapping the next iteration.  Swap-ins: H2D
+  // on the copy stream during this iteration's forward; the scatter kernel
+  // runs at the start of the next iteration (the restored request cannot be
+  // batched earlier: it leaves the swap queue only after this iteration).
+  struct SwapBuf {
+    f16* stage = nullptr;
+    SwapDesc* desc_dev = nullptr;
+    std::int32_t* prefix_dev = nullptr;
+    SwapDesc* desc_host = nullptr;      // pinned
+    std::int32_t* prefix_host = nullptr;  // pinned
+    cudaEvent_t copied = nullptr;       // H2D (in) / D2H (out) finished on the copy stream
+    cudaEvent_t consumed = nullptr;     // scatter (in) / gather (out) finished on the compute stream
+  };
+  struct PendingIn {
+    int buf, n_ops, tokens;
+  };
+  static constexpr int kMaxSwapOps = 4096;
+  SwapBuf in_[2], out_[2];
+  int in_next_ = 0, out_next_ = 0;
+  std::vector<PendingIn> pending_in_;
   std::int64_t stage_tokens_ = 0;
-  SwapDesc* swap_dev_ = nullptr;
-  std::int32_t* swap_prefix_dev_ = nullptr;
+  bool overlap_swaps_ = true;
+  void flush_swap_ins();
+  double swap_ms_ = 0.0;
+  double swap_bytes_timed_ = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> swap_ev_pending_;
+  std::vector<double> swap_ev_bytes_;
+  cudaEvent_t new_timing_event();
+  // sampled ids streamed to pinned host memory every iteration (the result
+  // a serving frontend would read)
+  std::int32_t* tok_host_[kRing] = {};
+  cudaEvent_t tok_done_[kRing] = {};
+  std::int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
+  cudaEvent_t mark_[2] = {};
+ public:
+  double timer(int op) override;
+ private:
 
   // host mirrors
   std::unordered_map<std::int64_t, int> slot_of_;
@@ -202,6 +237,7 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   IB2_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   record_ = pj.value("record", false);
   timing_ = pj.value("timing", false);
+  force_row_attention_ = pj.value("row_attention", false);
 
   max_slots_ = pj.value("max_requests", 1024);
   max_rows_ = pj.value("max_rows", 4096);
@@ -225,15 +261,16 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
     host_bytes_ = static_cast<std::size_t>(cpu / m_cost * static_cast<double>(M) * 1.25) + (64u << 20);
   }
   stage_tokens_ = pj.value("stage_tokens", 4096);
+  overlap_swaps_ = pj.value("overlap_swaps", true);
 
   // weights
-  weights_ = dalloc<bf16>(wl_.total);
+  weights_ = dalloc<f16>(wl_.total);
   for (const auto& it : wl_.items) launch_init_tensor(weights_ + it.off, it.count, spec_.weight_seed, it.id, it.kind, main_);
 
   // KV pool and block tables
   const std::int64_t pool_elems = spec_.layers * gpu_blocks_ * 2LL * spec_.d_model * kBlockTokens;
-  pool_ = dalloc<bf16>(pool_elems);
-  IB2_CUDA(cudaMemsetAsync(pool_, 0, pool_elems * sizeof(bf16), main_));
+  pool_ = dalloc<f16>(pool_elems);
+  IB2_CUDA(cudaMemsetAsync(pool_, 0, pool_elems * sizeof(f16), main_));
   table_ = dalloc<std::int32_t>(static_cast<std::size_t>(max_slots_) * max_lb_);
   launch_fill_i32(table_, static_cast<std::int64_t>(max_slots_) * max_lb_, -1, main_);
   stack_ = dalloc<std::int32_t>(gpu_blocks_ + 16);
@@ -268,11 +305,11 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   // activations (every GEMM A operand buffer has max_rows rows)
   const std::int64_t D = spec_.d_model;
   x_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * D);
-  xn_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
-  qkv_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * 3 * D);
-  attn_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
-  hid_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * spec_.ffn);
-  lmrows_ = dalloc<bf16>(static_cast<std::size_t>(max_rows_) * D);
+  xn_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * D);
+  qkv_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * 3 * D);
+  attn_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * D);
+  hid_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * spec_.ffn);
+  lmrows_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * D);
   logits_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.vocab);
   out_tok_ = dalloc<std::int32_t>(max_rows_);
   const int max_splits = (max_ctx_ + 255) / 256;
@@ -287,14 +324,24 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
     IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[i]), plan_bytes_, cudaHostAllocDefault));
     plan_dev_[i] = dalloc<unsigned char>(plan_bytes_);
     IB2_CUDA(cudaEventCreateWithFlags(&plan_done_[i], cudaEventDisableTiming));
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&tok_host_[i]), static_cast<std::size_t>(max_rows_) * 4, 0));
+    IB2_CUDA(cudaEventCreateWithFlags(&tok_done_[i], cudaEventDisableTiming));
   }
+  IB2_CUDA(cudaEventCreate(&mark_[0]));
+  IB2_CUDA(cudaEventCreate(&mark_[1]));
 
   // swap path
   IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_bytes_, cudaHostAllocDefault));
   arena_.reset(host_bytes_);
-  stage_ = dalloc<bf16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
-  swap_dev_ = dalloc<SwapDesc>(4096);
-  swap_prefix_dev_ = dalloc<std::int32_t>(4097);
+  for (SwapBuf* b : {&in_[0], &in_[1], &out_[0], &out_[1]}) {
+    b->stage = dalloc<f16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
+    b->desc_dev = dalloc<SwapDesc>(kMaxSwapOps);
+    b->prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 1);
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->desc_host), kMaxSwapOps * sizeof(SwapDesc), 0));
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->prefix_host), (kMaxSwapOps + 1) * 4, 0));
+    IB2_CUDA(cudaEventCreateWithFlags(&b->copied, cudaEventDisableTiming));
+    IB2_CUDA(cudaEventCreateWithFlags(&b->consumed, cudaEventDisableTiming));
+  }
   IB2_CUDA(cudaStreamSynchronize(main_));
 }
 
@@ -312,10 +359,23 @@ Impl::~Impl() {
     cudaFreeHost(plan_host_[i]);
     cudaFree(plan_dev_[i]);
     cudaEventDestroy(plan_done_[i]);
+    cudaFreeHost(tok_host_[i]);
+    cudaEventDestroy(tok_done_[i]);
   }
+  cudaEventDestroy(mark_[0]);
+  cudaEventDestroy(mark_[1]);
   cudaFreeHost(host_pool_);
+  for (SwapBuf* b : {&in_[0], &in_[1], &out_[0], &out_[1]}) {
+    cudaFree(b->stage);
+    cudaFree(b->desc_dev);
+    cudaFree(b->prefix_dev);
+    cudaFreeHost(b->desc_host);
+    cudaFreeHost(b->prefix_host);
+    cudaEventDestroy(b->copied);
+    cudaEventDestroy(b->consumed);
+  }
   void* ptrs[] = {weights_, pool_, table_, stack_, top_, err_, hist_, rope_cs_, x_, xn_, qkv_, attn_, hid_, lmrows_,
-                  logits_, out_tok_, part_o_, part_ml_, stage_, swap_dev_, swap_prefix_dev_};
+                  logits_, out_tok_, part_o_, part_ml_};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   cudaStreamDestroy(main_);
@@ -400,13 +460,26 @@ void Impl::apply_ops(const isim_batch_plan& p, int phase, std::vector<std::int32
   }
 }
 
+void Impl::flush_swap_ins() {
+  for (const PendingIn& p : pending_in_) {
+    SwapBuf& b = in_[p.buf];
+    IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));
+    IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, p.n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
+    IB2_CUDA(cudaMemcpyAsync(b.prefix_dev, b.prefix_host, (p.n_ops + 1) * 4, cudaMemcpyHostToDevice, main_));
+    launch_swap_copy(b.desc_dev, b.prefix_dev, p.n_ops, p.tokens, geom(), b.stage, false, main_);
+    ++kernel_launches_;
+    IB2_CUDA(cudaEventRecord(b.consumed, main_));
+  }
+  pending_in_.clear();
+}
+
 void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std::int64_t>& req_of, bool swap_in) {
   if (in_ops.empty()) return;
   const std::int64_t D = spec_.d_model, L = spec_.layers;
-  const std::size_t row_bytes = static_cast<std::size_t>(2 * D) * sizeof(bf16);
-  // Split ops at extent boundaries (swap-in) and into staging-sized batches.
+  const std::size_t row_bytes = static_cast<std::size_t>(2 * D) * sizeof(f16);
+  // Split ops at host-extent boundaries (swap-in) and at the staging size.
   std::vector<SwapDesc> ops;
-  std::vector<std::pair<std::int64_t, std::size_t>> ext_of;  // (request, extent index) per op (swap-in)
+  std::vector<std::pair<std::int64_t, std::size_t>> ext_of;  // (request, extent index)
   for (std::size_t i = 0; i < in_ops.size(); ++i) {
     const SwapDesc& o = in_ops[i];
     if (!swap_in) {
@@ -436,53 +509,85 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
   while (first < ops.size()) {
     std::size_t last = first;
     std::int64_t tok = 0;
-    while (last < ops.size() && tok + ops[last].n <= stage_tokens_ && last - first < 4096) tok += ops[last++].n;
-    std::vector<SwapDesc> batch(ops.begin() + first, ops.begin() + last);
-    std::vector<std::int32_t> prefix(batch.size() + 1, 0);
+    while (last < ops.size() && tok + ops[last].n <= stage_tokens_ && last - first < kMaxSwapOps) tok += ops[last++].n;
+    const int n_ops = static_cast<int>(last - first);
+    SwapBuf& b = swap_in ? in_[in_next_] : out_[out_next_];
+    const int bi = swap_in ? in_next_ : out_next_;
+    if (swap_in) in_next_ ^= 1;
+    else out_next_ ^= 1;
+    // The pinned descriptor arrays of this buffer were last uploaded two uses
+    // ago; make sure that upload (and the kernel reading them) is done.
+    IB2_CUDA(cudaEventSynchronize(b.consumed));
     std::int64_t off = 0;
-    for (std::size_t k = 0; k < batch.size(); ++k) {
-      batch[k].stage_off = off;
-      off += static_cast<std::int64_t>(batch[k].n) * L * 2 * D;
-      prefix[k + 1] = prefix[k] + batch[k].n;
+    b.prefix_host[0] = 0;
+    for (int k = 0; k < n_ops; ++k) {
+      b.desc_host[k] = ops[first + k];
+      b.desc_host[k].stage_off = off;
+      off += static_cast<std::int64_t>(b.desc_host[k].n) * L * 2 * D;
+      b.prefix_host[k + 1] = b.prefix_host[k] + b.desc_host[k].n;
     }
-    IB2_CUDA(cudaMemcpyAsync(swap_dev_, batch.data(), batch.size() * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
-    IB2_CUDA(cudaMemcpyAsync(swap_prefix_dev_, prefix.data(), prefix.size() * 4, cudaMemcpyHostToDevice, main_));
+    const int tokens = b.prefix_host[n_ops];
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (timing_) {
+      t0 = new_timing_event();
+      t1 = new_timing_event();
+    }
+    const double batch_bytes = static_cast<double>(tokens) * static_cast<double>(L) * static_cast<double>(row_bytes);
     if (swap_in) {
-      for (std::size_t k = 0; k < batch.size(); ++k) {
+      IB2_CUDA(cudaStreamWaitEvent(copy_, b.consumed, 0));  // staging free again
+      if (t0) IB2_CUDA(cudaEventRecord(t0, copy_));
+      for (int k = 0; k < n_ops; ++k) {
         const Extent& x = extents_[ext_of[first + k].first][ext_of[first + k].second];
         const std::int64_t n0 = x.hi0 - x.lo0;
-        const unsigned char* src = host_pool_ + x.off + static_cast<std::size_t>(batch[k].pos0 - x.lo0) * row_bytes;
-        IB2_CUDA(cudaMemcpy2DAsync(stage_ + batch[k].stage_off, static_cast<std::size_t>(batch[k].n) * row_bytes, src,
-                                   static_cast<std::size_t>(n0) * row_bytes,
-                                   static_cast<std::size_t>(batch[k].n) * row_bytes, L, cudaMemcpyHostToDevice, main_));
+        const unsigned char* src = host_pool_ + x.off + static_cast<std::size_t>(b.desc_host[k].pos0 - x.lo0) * row_bytes;
+        IB2_CUDA(cudaMemcpy2DAsync(b.stage + b.desc_host[k].stage_off, static_cast<std::size_t>(b.desc_host[k].n) * row_bytes,
+                                   src, static_cast<std::size_t>(n0) * row_bytes,
+                                   static_cast<std::size_t>(b.desc_host[k].n) * row_bytes, L, cudaMemcpyHostToDevice,
+                                   copy_));
+        extents_[ext_of[first + k].first][ext_of[first + k].second].lo = b.desc_host[k].pos0 + b.desc_host[k].n;
       }
-      launch_swap_copy(swap_dev_, swap_prefix_dev_, static_cast<int>(batch.size()), prefix.back(), geom(), stage_,
-                       false, main_);
-      ++kernel_launches_;
-      // Retire consumed host positions; free fully consumed extents.
-      for (std::size_t k = 0; k < batch.size(); ++k) {
-        auto& exts = extents_[ext_of[first + k].first];
-        Extent& x = exts[ext_of[first + k].second];
-        x.lo = batch[k].pos0 + batch[k].n;
+      IB2_CUDA(cudaEventRecord(b.copied, copy_));
+      if (t1) {
+        IB2_CUDA(cudaEventRecord(t1, copy_));
+        swap_ev_pending_.push_back({t0, t1});
+        swap_ev_bytes_.push_back(batch_bytes);
       }
+      pending_in_.push_back({bi, n_ops, tokens});
+      // Only the final batch of an iteration may stay in flight.
+      if (last < ops.size() || !overlap_swaps_) flush_swap_ins();
     } else {
-      launch_swap_copy(swap_dev_, swap_prefix_dev_, static_cast<int>(batch.size()), prefix.back(), geom(), stage_,
-                       true, main_);
+      IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));  // previous D2H out of this staging done
+      IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
+      IB2_CUDA(cudaMemcpyAsync(b.prefix_dev, b.prefix_host, (n_ops + 1) * 4, cudaMemcpyHostToDevice, main_));
+      launch_swap_copy(b.desc_dev, b.prefix_dev, n_ops, tokens, geom(), b.stage, true, main_);
       ++kernel_launches_;
-      for (std::size_t k = 0; k < batch.size(); ++k) {
-        const std::size_t bytes = static_cast<std::size_t>(batch[k].n) * L * row_bytes;
+      IB2_CUDA(cudaEventRecord(b.consumed, main_));
+      IB2_CUDA(cudaStreamWaitEvent(copy_, b.consumed, 0));
+      if (t0) IB2_CUDA(cudaEventRecord(t0, copy_));
+      for (int k = 0; k < n_ops; ++k) {
+        const std::size_t bytes = static_cast<std::size_t>(b.desc_host[k].n) * L * row_bytes;
         const std::size_t hoff = arena_.alloc(bytes);
-        IB2_CUDA(cudaMemcpyAsync(host_pool_ + hoff, stage_ + batch[k].stage_off, bytes, cudaMemcpyDeviceToHost, main_));
-        extents_[ext_of[first + k].first].push_back(
-            {batch[k].pos0, batch[k].pos0 + batch[k].n, batch[k].pos0, batch[k].pos0 + batch[k].n, hoff, bytes});
+        IB2_CUDA(cudaMemcpyAsync(host_pool_ + hoff, b.stage + b.desc_host[k].stage_off, bytes, cudaMemcpyDeviceToHost,
+                                 copy_));
+        extents_[ext_of[first + k].first].push_back({b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n,
+                                                     b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n, hoff,
+                                                     bytes});
       }
+      IB2_CUDA(cudaEventRecord(b.copied, copy_));
+      if (t1) {
+        IB2_CUDA(cudaEventRecord(t1, copy_));
+        swap_ev_pending_.push_back({t0, t1});
+        swap_ev_bytes_.push_back(batch_bytes);
+      }
+      if (!overlap_swaps_) IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));
     }
     first = last;
   }
   if (swap_in) {
-    // Host memory of consumed extents is reused only by later D2H copies on
-    // this same stream, which are ordered after the H2D reads above.
+    // Fully consumed extents go back to the arena; later D2H copies into that
+    // memory are queued behind these H2D reads on the same copy stream.
     for (const auto& [rid, idx] : ext_of) {
+      (void)idx;
       auto& exts = extents_[rid];
       for (std::size_t e = 0; e < exts.size();) {
         if (exts[e].lo >= exts[e].hi) {
@@ -516,8 +621,8 @@ void Impl::consume(const isim_batch_plan& p) {
     if (sp.pos + sp.count > max_ctx_) throw DeviceError("executor: row position beyond max_ctx");
     for (int k = 0; k < sp.count; ++k)
       rows.push_back({slot, sp.pos + k, sp.kind == ISIM_SPAN_FRESH ? 1 : 0, 0, sp.request_id});
-    if (sp.count == 1) {
-      drows.push_back(r0);
+    if (sp.count == 1 || force_row_attention_) {
+      for (int k = 0; k < sp.count; ++k) drows.push_back(r0 + k);
     } else {
       for (int k = 0; k < sp.count; k += 64) tiles.push_back({r0 + k, std::min(64, sp.count - k), slot, sp.pos + k});
     }
@@ -552,8 +657,10 @@ void Impl::consume(const isim_batch_plan& p) {
   const std::int32_t* d_allocs0 = reinterpret_cast<const std::int32_t*>(put(allocs0.data(), allocs0.size() * 4));
   IB2_CUDA(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, main_));
   IB2_CUDA(cudaEventRecord(plan_done_[k], main_));
+  h2d_bytes_ += static_cast<std::int64_t>(off);
 
-  // ---- pre-phase: block table, swap-in ------------------------------------------
+  // ---- pre-phase: last iteration's swap-in scatter, block table, swap-in H2D ----
+  flush_swap_ins();
   launch_block_update(table_, stack_, top_, err_, d_frees0, static_cast<int>(frees0.size()), d_allocs0,
                       static_cast<int>(allocs0.size()), main_);
   run_swaps(sw_in, sw_in_req, true);
@@ -571,6 +678,12 @@ void Impl::consume(const isim_batch_plan& p) {
     max_pos1_ = 0;
     for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
     forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(tiles.size()), static_cast<int>(samples.size()));
+    if (!samples.empty() && !record_) {
+      IB2_CUDA(cudaEventSynchronize(tok_done_[k]));
+      IB2_CUDA(cudaMemcpyAsync(tok_host_[k], out_tok_, samples.size() * 4, cudaMemcpyDeviceToHost, main_));
+      IB2_CUDA(cudaEventRecord(tok_done_[k], main_));
+      d2h_bytes_ += static_cast<std::int64_t>(samples.size()) * 4;
+    }
   }
 
   // ---- post-phase: swap-out gather + D2H, then frees -----------------------------
@@ -587,6 +700,7 @@ void Impl::consume(const isim_batch_plan& p) {
     IB2_CUDA(cudaEventSynchronize(plan_done_[k2]));
     std::memcpy(plan_host_[k2], frees1.data(), frees1.size() * 4);
     IB2_CUDA(cudaMemcpyAsync(plan_dev_[k2], plan_host_[k2], frees1.size() * 4, cudaMemcpyHostToDevice, main_));
+    h2d_bytes_ += static_cast<std::int64_t>(frees1.size()) * 4;
     IB2_CUDA(cudaEventRecord(plan_done_[k2], main_));
     launch_block_update(table_, stack_, top_, err_, reinterpret_cast<const std::int32_t*>(plan_dev_[k2]),
                         static_cast<int>(frees1.size()), nullptr, 0, main_);
@@ -614,6 +728,8 @@ void Impl::consume(const isim_batch_plan& p) {
   for (const auto& s : sw_in) swap_in_tok_ += s.n;
   for (const auto& s : sw_out) swap_out_tok_ += s.n;
   if (record_) {
+    flush_swap_ins();
+    IB2_CUDA(cudaStreamSynchronize(copy_));
     IB2_CUDA(cudaStreamSynchronize(main_));
     check_error();
     last_tok_.assign(p.n_spans, -1);
@@ -634,7 +750,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
   const int D = m.d_model, F = m.ffn;
   const KvGeom g = geom();
   const bool rms = m.family == Family::Llama;
-  auto gemm = [&](const bf16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias, bf16* out, int ldo,
+  auto gemm = [&](const f16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias, f16* out, int ldo,
                   float* outf, int ldf, int M) {
     GemmArgs ga{a, weights_ + w, M, N, K, epi, W(bias), out, ldo, outf, ldf};
     launch_gemm(ga, main_);
@@ -646,7 +762,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
   for (int l = 0; l < m.layers; ++l) {
     const LayerWeights& lw = wl_.layer[l];
     launch_norm(x_, D, nullptr, n, D, W(lw.ln1_g), W(lw.ln1_b), rms, m.norm_eps, xn_, D, main_);
-    gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreBf16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
+    gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreF16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
     launch_rope_kv_write(qkv_, rows_dev_, n, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, main_);
     kernel_launches_ += 2;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -675,16 +791,16 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
     if (m.parallel_residual()) {
       // GPT-J: x += attn W_o + mlp(ln1(x)); both read the same xn.
       gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
-      gemm(xn_, lw.w_in, F, D, Epi::GeluBf16, lw.b_in, hid_, F, nullptr, 0, n);
+      gemm(xn_, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid_, F, nullptr, 0, n);
       gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
     } else {
       gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
       launch_norm(x_, D, nullptr, n, D, W(lw.ln2_g), W(lw.ln2_b), rms, m.norm_eps, xn_, D, main_);
       ++kernel_launches_;
       if (m.family == Family::Llama)
-        gemm(xn_, lw.w_in, 2 * F, D, Epi::SwiGluBf16, -1, hid_, F, nullptr, 0, n);
+        gemm(xn_, lw.w_in, 2 * F, D, Epi::SwiGluF16, -1, hid_, F, nullptr, 0, n);
       else
-        gemm(xn_, lw.w_in, F, D, Epi::GeluBf16, lw.b_in, hid_, F, nullptr, 0, n);
+        gemm(xn_, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid_, F, nullptr, 0, n);
       gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
     }
   }
@@ -704,6 +820,7 @@ void Impl::check_error() {
 
 void Impl::sync() {
   IB2_CUDA(cudaSetDevice(dev_));
+  flush_swap_ins();
   IB2_CUDA(cudaStreamSynchronize(main_));
   IB2_CUDA(cudaStreamSynchronize(copy_));
   check_error();
@@ -717,6 +834,46 @@ void Impl::sync() {
   }
   ev_pending_.clear();
   ev_bytes_.clear();
+  for (std::size_t i = 0; i < swap_ev_pending_.size(); ++i) {
+    float ms = 0.f;
+    IB2_CUDA(cudaEventElapsedTime(&ms, swap_ev_pending_[i].first, swap_ev_pending_[i].second));
+    swap_ms_ += ms;
+    swap_bytes_timed_ += swap_ev_bytes_[i];
+    ev_free_.push_back(swap_ev_pending_[i]);
+  }
+  swap_ev_pending_.clear();
+  swap_ev_bytes_.clear();
+}
+
+cudaEvent_t Impl::new_timing_event() {
+  // Events come in pairs from the shared free list; split a pair if needed.
+  static thread_local std::vector<cudaEvent_t> spare;
+  if (spare.empty()) {
+    if (ev_free_.empty()) {
+      cudaEvent_t a, b;
+      IB2_CUDA(cudaEventCreate(&a));
+      IB2_CUDA(cudaEventCreate(&b));
+      ev_free_.push_back({a, b});
+    }
+    spare.push_back(ev_free_.back().first);
+    spare.push_back(ev_free_.back().second);
+    ev_free_.pop_back();
+  }
+  cudaEvent_t e = spare.back();
+  spare.pop_back();
+  return e;
+}
+
+double Impl::timer(int op) {
+  IB2_CUDA(cudaSetDevice(dev_));
+  if (op == 0 || op == 1) {
+    IB2_CUDA(cudaEventRecord(mark_[op], main_));
+    return 0.0;
+  }
+  IB2_CUDA(cudaEventSynchronize(mark_[1]));
+  float ms = 0.f;
+  IB2_CUDA(cudaEventElapsedTime(&ms, mark_[0], mark_[1]));
+  return ms;
 }
 
 std::string Impl::stats_json() const {
@@ -738,6 +895,11 @@ std::string Impl::stats_json() const {
   j["k1_ms"] = k1_ms_;
   j["k1_bytes"] = k1_bytes_timed_;
   j["gemm"] = gemm_uses_tcgen05() ? "tcgen05" : "simt";
+  j["h2d_bytes"] = h2d_bytes_;
+  j["d2h_bytes"] = d2h_bytes_;
+  j["swap_ms"] = swap_ms_;
+  j["swap_bytes_timed"] = swap_bytes_timed_;
+  j["kv_bytes_per_token"] = spec_.kv_bytes_per_token();
   return j.dump();
 }
 
@@ -779,11 +941,12 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
   const std::int64_t D = spec_.d_model, L = spec_.layers, H = spec_.heads, hd = spec_.head_dim();
   const std::int64_t n = hi - lo;
   if (cap < n * L * 2 * D * 2) throw DeviceError("read_kv: buffer too small");
+  IB2_CUDA(cudaStreamSynchronize(copy_));
   IB2_CUDA(cudaStreamSynchronize(main_));
   std::vector<std::int32_t> t(max_lb_);
   IB2_CUDA(cudaMemcpy(t.data(), table_ + static_cast<std::int64_t>(it->second) * max_lb_, max_lb_ * 4,
                       cudaMemcpyDeviceToHost));
-  bf16* dst = static_cast<bf16*>(out);
+  f16* dst = static_cast<f16*>(out);
   const KvGeom g = geom();
   const std::size_t row = static_cast<std::size_t>(2 * D) * 2;
   const auto ex = extents_.find(rid);
@@ -793,7 +956,7 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
       for (const Extent& x : ex->second)
         if (x.lo <= p && p < x.hi) on_host = &x;
     for (std::int64_t l = 0; l < L; ++l) {
-      bf16* d = dst + (l * n + (p - lo)) * 2 * D;
+      f16* d = dst + (l * n + (p - lo)) * 2 * D;
       if (on_host) {
         const std::int64_t n0 = on_host->hi0 - on_host->lo0;
         std::memcpy(d, host_pool_ + on_host->off + (static_cast<std::size_t>(l * n0 + (p - on_host->lo0))) * row, row);
@@ -803,7 +966,7 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
       if (pb < 0) throw DeviceError("read_kv: position neither on the GPU nor on the host");
       for (int kv = 0; kv < 2; ++kv)
         for (std::int64_t h = 0; h < H; ++h) {
-          const bf16* src = pool_ + l * g.layer_stride() + static_cast<std::int64_t>(pb) * g.block_stride() +
+          const f16* src = pool_ + l * g.layer_stride() + static_cast<std::int64_t>(pb) * g.block_stride() +
                             ((kv * H + h) * kBlockTokens + p % kBlockTokens) * hd;
           IB2_CUDA(cudaMemcpy(d + kv * D + h * hd, src, hd * 2, cudaMemcpyDeviceToHost));
         }

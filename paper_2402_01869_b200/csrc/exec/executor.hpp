@@ -28,6 +28,9 @@ class B200Executor : public PlanSink {
   virtual std::int64_t last_logits(float* out, std::int64_t cap) const = 0;
   virtual std::int32_t block_table(std::int64_t request_id, std::int32_t* out, std::int32_t cap) const = 0;
   virtual std::int64_t free_blocks() const = 0;
+  // op 0 / 1: record the start / stop mark on the compute stream;
+  // op 2: wait for the stop mark and return the elapsed device milliseconds.
+  virtual double timer(int op) = 0;
   virtual void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out,
                        std::int64_t cap) const = 0;
 };

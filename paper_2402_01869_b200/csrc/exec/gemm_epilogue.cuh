@@ -19,24 +19,24 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n0,
   float v[CNT];
 #pragma unroll
   for (int i = 0; i < CNT; ++i) v[i] = acc[i];
-  if (a.bias && a.epi != Epi::SwiGluBf16) {
+  if (a.bias && a.epi != Epi::SwiGluF16) {
 #pragma unroll
     for (int i = 0; i < CNT; ++i)
-      if (n0 + i < a.N) v[i] += __bfloat162float(a.bias[n0 + i]);
+      if (n0 + i < a.N) v[i] += __half2float(a.bias[n0 + i]);
   }
   switch (a.epi) {
-    case Epi::StoreBf16:
-    case Epi::GeluBf16: {
-      bf16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0;
+    case Epi::StoreF16:
+    case Epi::GeluF16: {
+      f16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0;
 #pragma unroll
       for (int i = 0; i < CNT; i += 2) {
         if (n0 + i >= a.N) break;
         float x0 = v[i], x1 = v[i + 1];
-        if (a.epi == Epi::GeluBf16) {
+        if (a.epi == Epi::GeluF16) {
           x0 = gelu_tanh(x0);
           x1 = gelu_tanh(x1);
         }
-        *reinterpret_cast<__nv_bfloat162*>(o + i) = __floats2bfloat162_rn(x0, x1);
+        *reinterpret_cast<__half2*>(o + i) = __floats2half2_rn(x0, x1);
       }
       break;
     }
@@ -54,11 +54,11 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n0,
         if (n0 + i < a.N) o[i] = v[i];
       break;
     }
-    case Epi::SwiGluBf16: {
-      bf16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0 / 2;
+    case Epi::SwiGluF16: {
+      f16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0 / 2;
 #pragma unroll
       for (int i = 0; i < CNT; i += 2)
-        if (n0 + i < a.N) o[i / 2] = __float2bfloat16_rn(silu(v[i]) * v[i + 1]);
+        if (n0 + i < a.N) o[i / 2] = __float2half_rn(silu(v[i]) * v[i + 1]);
       break;
     }
   }

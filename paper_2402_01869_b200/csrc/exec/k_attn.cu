@@ -10,7 +10,7 @@
 // K2 (chunk rows: prefill / recompute / API-returned tokens): 64-query tiles
 // of one request and one head; K and V tiles of 64 positions (4 paged blocks)
 // are staged in XOR-swizzled shared memory with cp.async and consumed by
-// bf16 tensor-core MMAs with an online softmax (causal mask by position).
+// f16 tensor-core MMAs with an online softmax (causal mask by position).
 // Keys are visited in the same ascending block order as K1.
 #include <cfloat>
 
@@ -24,11 +24,11 @@ constexpr int kSplit = 256;       // positions per K1 CTA
 constexpr int kDecWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+__device__ __forceinline__ void h8_to_f32(const uint4& u, float* f) {
+  const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const float2 t = __bfloat1622float2(h[i]);
+    const float2 t = __half22float2(h[i]);
     f[2 * i] = t.x;
     f[2 * i + 1] = t.y;
   }
@@ -36,8 +36,8 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 
 template <int HD>
 __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
-    const bf16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
-    const bf16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
+    const f16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
+    const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
     const std::int32_t* __restrict__ table, int max_lb, int H, int max_splits, float* __restrict__ part_o,
     float* __restrict__ part_ml) {
   constexpr int LPT = HD / 8;   // lanes per token
@@ -60,19 +60,19 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
   float q[8];
   {
     const uint4 u = *reinterpret_cast<const uint4*>(qkv + static_cast<std::int64_t>(r) * 3 * D + h * HD + c * 8);
-    bf16x8_to_f32(u, q);
+    h8_to_f32(u, q);
     const float sc = rsqrtf(static_cast<float>(HD)) * kLog2e;
 #pragma unroll
     for (int i = 0; i < 8; ++i) q[i] *= sc;
   }
   const std::int32_t* tab = table + static_cast<std::int64_t>(d.slot) * max_lb;
-  const bf16* base = pool + layer_off;
+  const f16* base = pool + layer_off;
   const int lb0 = start / kBlockTokens, lb1 = (end - 1) / kBlockTokens;
 
   // Pass 1: scores.
   float mx = -FLT_MAX;
   for (int lb = lb0 + warp; lb <= lb1; lb += kDecWarps) {
-    const bf16* kblk = base + static_cast<std::int64_t>(tab[lb]) * block_stride + (static_cast<std::int64_t>(h) * kBlockTokens) * HD;
+    const f16* kblk = base + static_cast<std::int64_t>(tab[lb]) * block_stride + (static_cast<std::int64_t>(h) * kBlockTokens) * HD;
     uint4 kv[kBlockTokens / TPW];
 #pragma unroll
     for (int t = 0; t < kBlockTokens / TPW; ++t)
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
 #pragma unroll
     for (int t = 0; t < kBlockTokens / TPW; ++t) {
       float kf[8];
-      bf16x8_to_f32(kv[t], kf);
+      h8_to_f32(kv[t], kf);
       float dot = 0.f;
 #pragma unroll
       for (int i = 0; i < 8; ++i) dot = fmaf(q[i], kf[i], dot);
@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
   // Pass 2: P * V.
   float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   for (int lb = lb0 + warp; lb <= lb1; lb += kDecWarps) {
-    const bf16* vblk = base + static_cast<std::int64_t>(tab[lb]) * block_stride +
+    const f16* vblk = base + static_cast<std::int64_t>(tab[lb]) * block_stride +
                        (static_cast<std::int64_t>(H + h) * kBlockTokens) * HD;
     uint4 vv[kBlockTokens / TPW];
 #pragma unroll
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
       const int p = lb * kBlockTokens + t * TPW + grp;
       const float w = (p >= start && p < end) ? s_score[p - start] : 0.f;
       float vf[8];
-      bf16x8_to_f32(vv[t], vf);
+      h8_to_f32(vv[t], vf);
 #pragma unroll
       for (int i = 0; i < 8; ++i) acc[i] = fmaf(w, vf[i], acc[i]);
     }
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
 
 __global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows, int H,
                                       int HD, int max_splits, const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml, bf16* __restrict__ out) {
+                                      const float* __restrict__ part_ml, f16* __restrict__ out) {
   const int dr = blockIdx.x, h = blockIdx.y;
   const int r = drow[dr];
   const int ns = (rows[r].pos + 1 + kSplit - 1) / kSplit;
@@ -171,7 +171,7 @@ __global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, con
   for (int i = threadIdx.x; i < HD; i += blockDim.x) {
     float o = 0.f;
     for (int s = 0; s < ns; ++s) o += part_o[(base + s) * HD + i] * exp2f(part_ml[(base + s) * 2] - M);
-    out[static_cast<std::int64_t>(r) * H * HD + h * HD + i] = __float2bfloat16_rn(o * inv);
+    out[static_cast<std::int64_t>(r) * H * HD + h * HD + i] = __float2half_rn(o * inv);
   }
 }
 
@@ -202,17 +202,17 @@ __device__ __forceinline__ void ldsm_x4_t(std::uint32_t addr, std::uint32_t& r0,
 __device__ __forceinline__ void mma16816(float* c, std::uint32_t a0, std::uint32_t a1, std::uint32_t a2,
                                          std::uint32_t a3, std::uint32_t b0, std::uint32_t b1) {
   asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
       "{%0,%1,%2,%3};\n"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-__device__ __forceinline__ std::uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+__device__ __forceinline__ std::uint32_t pack_f16(float lo, float hi) {
+  const __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const std::uint32_t*>(&v);
 }
 
-// Swizzled element offset of (row, col) in a [rows][HD] bf16 tile.
+// Swizzled element offset of (row, col) in a [rows][HD] f16 tile.
 template <int HD>
 __device__ __forceinline__ int swz(int row, int col) {
   const int chunk = (col >> 3) ^ (row & 7);
@@ -222,29 +222,29 @@ __device__ __forceinline__ int swz(int row, int col) {
 constexpr int kTileQ = 64, kTileK = 64;
 
 template <int HD>
-__global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict__ qkv,
+__global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__ qkv,
                                                          const TileDesc* __restrict__ tiles,
-                                                         const bf16* __restrict__ pool, std::int64_t layer_off,
+                                                         const f16* __restrict__ pool, std::int64_t layer_off,
                                                          std::int64_t block_stride,
                                                          const std::int32_t* __restrict__ table, int max_lb, int H,
-                                                         bf16* __restrict__ out) {
+                                                         f16* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  bf16* sQ = reinterpret_cast<bf16*>(smem_raw);
-  bf16* sK = sQ + kTileQ * HD;
-  bf16* sV = sK + kTileK * HD;
+  f16* sQ = reinterpret_cast<f16*>(smem_raw);
+  f16* sK = sQ + kTileQ * HD;
+  f16* sV = sK + kTileK * HD;
   const TileDesc td = tiles[blockIdx.x];
   const int h = blockIdx.y;
   const int D = H * HD;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const std::int32_t* tab = table + static_cast<std::int64_t>(td.slot) * max_lb;
   const int last_pos = td.pos0 + td.nrows - 1;
-  const bf16* base = pool + layer_off;
+  const f16* base = pool + layer_off;
 
   // Q tile (rows beyond nrows load zeros).
   for (int i = tid; i < kTileQ * (HD / 8); i += 128) {
     const int row = i / (HD / 8), ch = i % (HD / 8);
     const bool ok = row < td.nrows;
-    const bf16* src = qkv + static_cast<std::int64_t>(td.row0 + (ok ? row : 0)) * 3 * D + h * HD + ch * 8;
+    const f16* src = qkv + static_cast<std::int64_t>(td.row0 + (ok ? row : 0)) * 3 * D + h * HD + ch * 8;
     cp_async16(smem_u32(sQ + swz<HD>(row, ch * 8)), src, ok);
   }
 
@@ -270,8 +270,8 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict_
       const bool ok = p <= last_pos;
       std::int64_t off = 0;
       if (ok) off = static_cast<std::int64_t>(tab[p / kBlockTokens]) * block_stride + (p % kBlockTokens) * HD + ch * 8;
-      const bf16* ksrc = base + off + (static_cast<std::int64_t>(h) * kBlockTokens) * HD;
-      const bf16* vsrc = base + off + (static_cast<std::int64_t>(H + h) * kBlockTokens) * HD;
+      const f16* ksrc = base + off + (static_cast<std::int64_t>(h) * kBlockTokens) * HD;
+      const f16* vsrc = base + off + (static_cast<std::int64_t>(H + h) * kBlockTokens) * HD;
       cp_async16(smem_u32(sK + swz<HD>(row, ch * 8)), ok ? ksrc : base, ok);
       cp_async16(smem_u32(sV + swz<HD>(row, ch * 8)), ok ? vsrc : base, ok);
     }
@@ -323,10 +323,12 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict_
     float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
-      s[j][0] = exp2f(s[j][0] - mx0);
-      s[j][1] = exp2f(s[j][1] - mx0);
-      s[j][2] = exp2f(s[j][2] - mx1);
-      s[j][3] = exp2f(s[j][3] - mx1);
+      // P enters the PV MMA as f16; normalize by the sum of the same rounded
+      // values so numerator and denominator agree.
+      s[j][0] = __half2float(__float2half_rn(exp2f(s[j][0] - mx0)));
+      s[j][1] = __half2float(__float2half_rn(exp2f(s[j][1] - mx0)));
+      s[j][2] = __half2float(__float2half_rn(exp2f(s[j][2] - mx1)));
+      s[j][3] = __half2float(__float2half_rn(exp2f(s[j][3] - mx1)));
       rs0 += s[j][0] + s[j][1];
       rs1 += s[j][2] + s[j][3];
     }
@@ -342,10 +344,10 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict_
     // O += P V
 #pragma unroll
     for (int ks = 0; ks < kTileK / 16; ++ks) {
-      const std::uint32_t a0 = pack_bf16(s[2 * ks][0], s[2 * ks][1]);
-      const std::uint32_t a1 = pack_bf16(s[2 * ks][2], s[2 * ks][3]);
-      const std::uint32_t a2 = pack_bf16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
-      const std::uint32_t a3 = pack_bf16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
+      const std::uint32_t a0 = pack_f16(s[2 * ks][0], s[2 * ks][1]);
+      const std::uint32_t a1 = pack_f16(s[2 * ks][2], s[2 * ks][3]);
+      const std::uint32_t a2 = pack_f16(s[2 * ks + 1][0], s[2 * ks + 1][1]);
+      const std::uint32_t a3 = pack_f16(s[2 * ks + 1][2], s[2 * ks + 1][3]);
 #pragma unroll
       for (int i = 0; i < DT; i += 2) {
         std::uint32_t b0, b1, b2, b3;
@@ -369,16 +371,16 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const bf16* __restrict_
   for (int i = 0; i < DT; ++i) {
     const int col = h * HD + i * 8 + 2 * t4;
     if (r0 < td.nrows)
-      *reinterpret_cast<__nv_bfloat162*>(out + static_cast<std::int64_t>(td.row0 + r0) * D + col) =
-          __floats2bfloat162_rn(o[i][0] * inv0, o[i][1] * inv0);
+      *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r0) * D + col) =
+          __floats2half2_rn(o[i][0] * inv0, o[i][1] * inv0);
     if (r1 < td.nrows)
-      *reinterpret_cast<__nv_bfloat162*>(out + static_cast<std::int64_t>(td.row0 + r1) * D + col) =
-          __floats2bfloat162_rn(o[i][2] * inv1, o[i][3] * inv1);
+      *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r1) * D + col) =
+          __floats2half2_rn(o[i][2] * inv1, o[i][3] * inv1);
   }
 }
 
 template <int HD>
-void launch_chunk_hd(const bf16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer, bf16* out,
+void launch_chunk_hd(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer, f16* out,
                      cudaStream_t s) {
   const int smem = (kTileQ + 2 * kTileK) * HD * 2;
   static bool configured = false;
@@ -393,8 +395,8 @@ void launch_chunk_hd(const bf16* qkv, const TileDesc* tiles, int n_tiles, const 
 }
 
 template <int HD>
-void launch_decode_hd(const bf16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
-                      int layer, int max_splits, float* part_o, float* part_ml, bf16* out, cudaStream_t s) {
+void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
+                      int layer, int max_splits, float* part_o, float* part_ml, f16* out, cudaStream_t s) {
   dim3 grid(max_splits, g.heads, n);
   decode_attn_kernel<HD><<<grid, kDecWarps * 32, 0, s>>>(qkv, drow, rows, g.pool, layer * g.layer_stride(),
                                                          g.block_stride(), g.table, g.max_lblocks, g.heads,
@@ -406,9 +408,9 @@ void launch_decode_hd(const bf16* qkv, const std::int32_t* drow, const RowDesc* 
 
 }  // namespace
 
-void launch_decode_attention(const bf16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
+void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
-                             bf16* out, cudaStream_t s) {
+                             f16* out, cudaStream_t s) {
   if (n_drows <= 0) return;
   const int max_splits = (max_pos_plus1 + kSplit - 1) / kSplit;
   switch (g.head_dim) {
@@ -419,8 +421,8 @@ void launch_decode_attention(const bf16* qkv, const std::int32_t* drow, const Ro
   }
 }
 
-void launch_chunk_attention(const bf16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
-                            bf16* out, cudaStream_t s) {
+void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
+                            f16* out, cudaStream_t s) {
   if (n_tiles <= 0) return;
   switch (g.head_dim) {
     case 64: launch_chunk_hd<64>(qkv, tiles, n_tiles, g, layer, out, s); break;

@@ -20,8 +20,8 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs a) {
     for (int i = threadIdx.x; i < BM * BK; i += 256) {
       const int r = i / BK, c = i % BK;
       const int m = m0 + r, n = n0 + r, k = k0 + c;
-      sA[c][r] = (m < a.M && k < a.K) ? __bfloat162float(a.a[static_cast<std::int64_t>(m) * a.K + k]) : 0.f;
-      sW[c][r] = (n < a.N && k < a.K) ? __bfloat162float(a.w[static_cast<std::int64_t>(n) * a.K + k]) : 0.f;
+      sA[c][r] = (m < a.M && k < a.K) ? __half2float(a.a[static_cast<std::int64_t>(m) * a.K + k]) : 0.f;
+      sW[c][r] = (n < a.N && k < a.K) ? __half2float(a.w[static_cast<std::int64_t>(n) * a.K + k]) : 0.f;
     }
     __syncthreads();
 #pragma unroll 8

@@ -1,6 +1,6 @@
 // K3: projection GEMM on 5th-generation tensor cores (sm_100a).
 //
-//   C[M][N] = A[M][K] . W[N][K]^T   (bf16 in, fp32 accumulate in TMEM)
+//   C[M][N] = A[M][K] . W[N][K]^T   (f16 in, fp32 accumulate in TMEM)
 //
 // Warp-specialized, one output tile (128 x BN) per CTA:
 //   warp 0      TMA producer: A and W tiles (128 B swizzle) into a STAGES-deep
@@ -76,8 +76,8 @@ __device__ __forceinline__ std::uint64_t smem_desc(const void* p) {
 template <int BN>
 __host__ __device__ constexpr std::uint32_t instr_desc() {
   return (1u << 4)                                     // D = f32
-         | (1u << 7)                                   // A = bf16
-         | (1u << 10)                                  // B = bf16
+         | (0u << 7)                                   // A = f16
+         | (0u << 10)                                  // B = f16
          | (static_cast<std::uint32_t>(BN >> 3) << 17) // N
          | (static_cast<std::uint32_t>(BM >> 4) << 24);// M
 }
@@ -208,14 +208,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map over [rows][K] (row stride ld elements), box 64 x box_rows.
+// 2-D f16 tensor map over [rows][K] (row stride ld elements), box 64 x box_rows.
 CUtensorMap make_map(const void* base, std::int64_t rows, int K, int ld, int box_rows) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
   const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
@@ -285,8 +285,8 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s) {
 
 void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, const void* bias, void* out, int ldo,
                 void* outf, int ldf, bool force_simt, void* stream) {
-  GemmArgs g{static_cast<const bf16*>(a), static_cast<const bf16*>(w), M, N, K, static_cast<Epi>(epi),
-             static_cast<const bf16*>(bias), static_cast<bf16*>(out), ldo, static_cast<float*>(outf), ldf};
+  GemmArgs g{static_cast<const f16*>(a), static_cast<const f16*>(w), M, N, K, static_cast<Epi>(epi),
+             static_cast<const f16*>(bias), static_cast<f16*>(out), ldo, static_cast<float*>(outf), ldf};
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const std::int64_t saved = g_a_rows_capacity;
   g_a_rows_capacity = 0;  // caller buffers are exactly M rows

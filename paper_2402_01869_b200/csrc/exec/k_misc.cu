@@ -29,11 +29,11 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-__global__ void init_tensor_kernel(bf16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind) {
+__global__ void init_tensor_kernel(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind) {
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
     float v = kind == 1 ? 1.0f : (kind == 2 ? 0.0f : synth_weight(seed, id, static_cast<std::uint64_t>(i)));
-    dst[i] = __float2bfloat16_rn(v);
+    dst[i] = __float2half_rn(v);
   }
 }
 
@@ -50,7 +50,7 @@ __global__ void fill_kernel(std::int32_t* p, std::int64_t n, std::int32_t v) {
 }
 
 __global__ void embed_kernel(const RowDesc* __restrict__ rows, std::int32_t* __restrict__ hist, int hist_stride,
-                             const bf16* __restrict__ tok_emb, const bf16* __restrict__ pos_emb, int D,
+                             const f16* __restrict__ tok_emb, const f16* __restrict__ pos_emb, int D,
                              std::uint64_t token_seed, int vocab, float* __restrict__ x) {
   const int r = blockIdx.x;
   const RowDesc d = rows[r];
@@ -67,12 +67,12 @@ __global__ void embed_kernel(const RowDesc* __restrict__ rows, std::int32_t* __r
     tok_s = t;
   }
   __syncthreads();
-  const bf16* e = tok_emb + static_cast<std::int64_t>(tok_s) * D;
-  const bf16* p = pos_emb ? pos_emb + static_cast<std::int64_t>(d.pos) * D : nullptr;
+  const f16* e = tok_emb + static_cast<std::int64_t>(tok_s) * D;
+  const f16* p = pos_emb ? pos_emb + static_cast<std::int64_t>(d.pos) * D : nullptr;
   float* xr = x + static_cast<std::int64_t>(r) * D;
   for (int i = threadIdx.x; i < D; i += blockDim.x) {
-    float v = __bfloat162float(e[i]);
-    if (p) v = __fadd_rn(v, __bfloat162float(p[i]));
+    float v = __half2float(e[i]);
+    if (p) v = __fadd_rn(v, __half2float(p[i]));
     xr[i] = v;
   }
 }
@@ -81,8 +81,8 @@ __global__ void embed_kernel(const RowDesc* __restrict__ rows, std::int32_t* __r
 template <int NT, int PER>
 __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, int ldx,
                                                   const std::int32_t* __restrict__ row_index, int D,
-                                                  const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
-                                                  int rms, float eps, bf16* __restrict__ y, int ldy) {
+                                                  const f16* __restrict__ gamma, const f16* __restrict__ beta,
+                                                  int rms, float eps, f16* __restrict__ y, int ldy) {
   __shared__ float red[NT / 32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -106,30 +106,30 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, i
   }
   const float var = block_sum<NT>(q, red) / D;
   const float inv = rsqrtf(var + eps);
-  bf16* yr = y + static_cast<std::int64_t>(r) * ldy;
+  f16* yr = y + static_cast<std::int64_t>(r) * ldy;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     const int c = threadIdx.x + i * NT;
     if (c < D) {
-      float o = (v[i] - mean) * inv * __bfloat162float(gamma[c]);
-      if (beta) o += __bfloat162float(beta[c]);
-      yr[c] = __float2bfloat16_rn(o);
+      float o = (v[i] - mean) * inv * __half2float(gamma[c]);
+      if (beta) o += __half2float(beta[c]);
+      yr[c] = __float2half_rn(o);
     }
   }
 }
 
 // Per row: rotate q and k of every head (fp32, no contraction, matching the
-// oracle's float32 arithmetic), round to bf16, and store k, v into the row's
+// oracle's float32 arithmetic), round to f16, and store k, v into the row's
 // paged slot.
-__global__ void rope_kv_kernel(bf16* __restrict__ qkv, const RowDesc* __restrict__ rows, bf16* __restrict__ pool,
+__global__ void rope_kv_kernel(f16* __restrict__ qkv, const RowDesc* __restrict__ rows, f16* __restrict__ pool,
                                std::int64_t layer_off, std::int64_t block_stride, const std::int32_t* __restrict__ table,
                                int max_lb, int H, int hd, int rot, int interleaved, const float* __restrict__ cs) {
   const int r = blockIdx.x;
   const RowDesc d = rows[r];
   const int D = H * hd;
-  bf16* row = qkv + static_cast<std::int64_t>(r) * 3 * D;
+  f16* row = qkv + static_cast<std::int64_t>(r) * 3 * D;
   const int pb = table[static_cast<std::int64_t>(d.slot) * max_lb + d.pos / kBlockTokens];
-  bf16* blk = pool + layer_off + static_cast<std::int64_t>(pb) * block_stride;
+  f16* blk = pool + layer_off + static_cast<std::int64_t>(pb) * block_stride;
   const int tok = d.pos % kBlockTokens;
   const int half = rot / 2;
   const float* c = cs + static_cast<std::int64_t>(d.pos) * rot;  // [half][2] = (cos, sin)
@@ -138,15 +138,15 @@ __global__ void rope_kv_kernel(bf16* __restrict__ qkv, const RowDesc* __restrict
     const int which = t / (H * half);  // 0 = q, 1 = k
     const int h = (t / half) % H;
     const int i = t % half;
-    bf16* base = row + which * D + h * hd;
+    f16* base = row + which * D + h * hd;
     const int ia = interleaved ? 2 * i : i;
     const int ib = interleaved ? 2 * i + 1 : i + half;
-    const float a = __bfloat162float(base[ia]), b = __bfloat162float(base[ib]);
+    const float a = __half2float(base[ia]), b = __half2float(base[ib]);
     const float co = c[2 * i], si = c[2 * i + 1];
     const float ra = __fsub_rn(__fmul_rn(a, co), __fmul_rn(b, si));
     const float rb = __fadd_rn(__fmul_rn(b, co), __fmul_rn(a, si));
-    base[ia] = __float2bfloat16_rn(ra);
-    base[ib] = __float2bfloat16_rn(rb);
+    base[ia] = __float2half_rn(ra);
+    base[ib] = __float2half_rn(rb);
   }
   __syncthreads();
   // k, v -> pool [kv][h][tok][hd], 16-byte vectors.
@@ -156,7 +156,7 @@ __global__ void rope_kv_kernel(bf16* __restrict__ qkv, const RowDesc* __restrict
     const int h = (t / vec) % H;
     const int j = t % vec;
     const uint4 val = *reinterpret_cast<const uint4*>(row + (1 + kv) * D + h * hd + j * 8);
-    bf16* dst = blk + ((static_cast<std::int64_t>(kv) * H + h) * kBlockTokens + tok) * hd + j * 8;
+    f16* dst = blk + ((static_cast<std::int64_t>(kv) * H + h) * kBlockTokens + tok) * hd + j * 8;
     *reinterpret_cast<uint4*>(dst) = val;
   }
 }
@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
   }
 }
 
-__global__ void gather_rows_kernel(const bf16* __restrict__ src, int ld, const std::int32_t* __restrict__ rows, int D,
-                                   bf16* __restrict__ dst) {
+__global__ void gather_rows_kernel(const f16* __restrict__ src, int ld, const std::int32_t* __restrict__ rows, int D,
+                                   f16* __restrict__ dst) {
   const int r = blockIdx.x;
   const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<std::int64_t>(rows[r]) * ld);
   uint4* d = reinterpret_cast<uint4*>(dst + static_cast<std::int64_t>(r) * D);
@@ -245,9 +245,9 @@ __global__ void __launch_bounds__(1024) block_update_kernel(std::int32_t* __rest
 // K7: one CTA per (swap token, layer); moves the token's 2*D k/v elements
 // between the paged pool and the op's [L][n][2D] staging slab.
 __global__ void swap_copy_kernel(const SwapDesc* __restrict__ ops, const std::int32_t* __restrict__ prefix, int n_ops,
-                                 bf16* __restrict__ pool, std::int64_t layer_stride, std::int64_t block_stride,
+                                 f16* __restrict__ pool, std::int64_t layer_stride, std::int64_t block_stride,
                                  const std::int32_t* __restrict__ table, int max_lb, int H, int hd,
-                                 bf16* __restrict__ stage, int to_stage) {
+                                 f16* __restrict__ stage, int to_stage) {
   const int t = blockIdx.x, layer = blockIdx.y;
   int lo = 0, hi = n_ops;  // find op with prefix[op] <= t < prefix[op+1]
   while (hi - lo > 1) {
@@ -260,8 +260,8 @@ __global__ void swap_copy_kernel(const SwapDesc* __restrict__ ops, const std::in
   const int pos = op.pos0 + i;
   const int D = H * hd;
   const int pb = table[static_cast<std::int64_t>(op.slot) * max_lb + pos / kBlockTokens];
-  bf16* blk = pool + layer * layer_stride + static_cast<std::int64_t>(pb) * block_stride;
-  bf16* srow = stage + op.stage_off + (static_cast<std::int64_t>(layer) * op.n + i) * 2 * D;
+  f16* blk = pool + layer * layer_stride + static_cast<std::int64_t>(pb) * block_stride;
+  f16* srow = stage + op.stage_off + (static_cast<std::int64_t>(layer) * op.n + i) * 2 * D;
   const int tok = pos % kBlockTokens;
   for (int v = threadIdx.x; v < 2 * D / 8; v += blockDim.x) {
     const int e = v * 8;
@@ -280,7 +280,7 @@ int grid_for(std::int64_t n, int threads) {
 
 }  // namespace
 
-void launch_init_tensor(bf16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
+void launch_init_tensor(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
                         cudaStream_t s) {
   init_tensor_kernel<<<grid_for(count, 256), 256, 0, s>>>(dst, count, seed, id, kind);
   IB2_LAUNCH_CHECK();
@@ -296,15 +296,15 @@ void launch_fill_i32(std::int32_t* p, std::int64_t n, std::int32_t v, cudaStream
   IB2_LAUNCH_CHECK();
 }
 
-void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_stride, const bf16* tok_emb,
-                  const bf16* pos_emb, int D, std::uint64_t token_seed, int vocab, float* x, cudaStream_t s) {
+void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_stride, const f16* tok_emb,
+                  const f16* pos_emb, int D, std::uint64_t token_seed, int vocab, float* x, cudaStream_t s) {
   if (n <= 0) return;
   embed_kernel<<<n, 256, 0, s>>>(rows, hist, hist_stride, tok_emb, pos_emb, D, token_seed, vocab, x);
   IB2_LAUNCH_CHECK();
 }
 
-void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, int D, const bf16* gamma,
-                 const bf16* beta, bool rms, float eps, bf16* y, int ldy, cudaStream_t s) {
+void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, int D, const f16* gamma,
+                 const f16* beta, bool rms, float eps, f16* y, int ldy, cudaStream_t s) {
   if (n <= 0) return;
   if (D <= 1024) {
     norm_kernel<256, 4><<<n, 256, 0, s>>>(x, ldx, row_index, D, gamma, beta, rms, eps, y, ldy);
@@ -316,7 +316,7 @@ void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, 
   IB2_LAUNCH_CHECK();
 }
 
-void launch_rope_kv_write(bf16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
+void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
                           bool interleaved, const float* rope_cs, cudaStream_t s) {
   if (n <= 0) return;
   rope_kv_kernel<<<n, 256, 0, s>>>(qkv, rows, g.pool, layer * g.layer_stride(), g.block_stride(), g.table,
@@ -331,7 +331,7 @@ void launch_argmax(const float* logits, int n, int V, const std::int32_t* sample
   IB2_LAUNCH_CHECK();
 }
 
-void launch_gather_rows(const bf16* src, int ld, const std::int32_t* rows, int n, int D, bf16* dst,
+void launch_gather_rows(const f16* src, int ld, const std::int32_t* rows, int n, int D, f16* dst,
                         cudaStream_t s) {
   if (n <= 0) return;
   gather_rows_kernel<<<n, 256, 0, s>>>(src, ld, rows, D, dst);
@@ -346,7 +346,7 @@ void launch_block_update(std::int32_t* table, std::int32_t* stack, std::int32_t*
 }
 
 void launch_swap_copy(const SwapDesc* ops, const std::int32_t* tok_prefix, int n_ops, int total_tokens,
-                      const KvGeom& g, bf16* stage, bool to_stage, cudaStream_t s) {
+                      const KvGeom& g, f16* stage, bool to_stage, cudaStream_t s) {
   if (total_tokens <= 0) return;
   dim3 grid(total_tokens, g.layers);
   swap_copy_kernel<<<grid, 256, 0, s>>>(ops, tok_prefix, n_ops, g.pool, g.layer_stride(), g.block_stride(),

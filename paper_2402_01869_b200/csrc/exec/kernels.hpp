@@ -9,7 +9,7 @@
 namespace ib2 {
 
 struct KvGeom {
-  bf16* pool;         // [L][num_blocks][2][H][16][hd]
+  f16* pool;         // [L][num_blocks][2][H][16][hd]
   std::int64_t num_blocks;
   int layers, heads, head_dim;
   const std::int32_t* table;  // [slots][max_lblocks]
@@ -19,31 +19,31 @@ struct KvGeom {
 };
 
 // init
-void launch_init_tensor(bf16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
+void launch_init_tensor(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
                         cudaStream_t s);
 void launch_iota_desc(std::int32_t* stack, std::int64_t n, cudaStream_t s);
 void launch_fill_i32(std::int32_t* p, std::int64_t n, std::int32_t v, cudaStream_t s);
 
 // K9: x[r] = E[tok] (+ P[pos]); history written for synthetic rows.
-void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_stride, const bf16* tok_emb,
-                  const bf16* pos_emb, int D, std::uint64_t token_seed, int vocab, float* x, cudaStream_t s);
+void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_stride, const f16* tok_emb,
+                  const f16* pos_emb, int D, std::uint64_t token_seed, int vocab, float* x, cudaStream_t s);
 
 // K5: y = norm(x) (LayerNorm with bias, or RMSNorm when beta == null && rms)
-void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, int D, const bf16* gamma,
-                 const bf16* beta, bool rms, float eps, bf16* y, int ldy, cudaStream_t s);
+void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, int D, const f16* gamma,
+                 const f16* beta, bool rms, float eps, f16* y, int ldy, cudaStream_t s);
 
 // K4: RoPE on q,k in place + write k,v of every row into the paged pool.
-void launch_rope_kv_write(bf16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
+void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
                           bool interleaved, const float* rope_cs, cudaStream_t s);
 
 // K1: split-KV paged decode attention for single rows.
-void launch_decode_attention(const bf16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
+void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
-                             bf16* out, cudaStream_t s);
+                             f16* out, cudaStream_t s);
 
 // K2: tiled causal attention over the paged prefix for chunk rows.
-void launch_chunk_attention(const bf16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
-                            bf16* out, cudaStream_t s);
+void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
+                            f16* out, cudaStream_t s);
 
 // K3: projection GEMM with fused epilogue.
 void launch_gemm(const GemmArgs& a, cudaStream_t s);
@@ -53,7 +53,7 @@ bool gemm_uses_tcgen05();
 void launch_argmax(const float* logits, int n, int V, const std::int32_t* sample_rows, const RowDesc* rows,
                    std::int32_t* hist, int hist_stride, std::int32_t* out_tok, cudaStream_t s);
 
-void launch_gather_rows(const bf16* src, int ld, const std::int32_t* rows, int n, int D, bf16* dst,
+void launch_gather_rows(const f16* src, int ld, const std::int32_t* rows, int n, int D, f16* dst,
                         cudaStream_t s);
 
 // K8: block-table update: frees pushed (LIFO), then allocs popped.
@@ -62,6 +62,6 @@ void launch_block_update(std::int32_t* table, std::int32_t* stack, std::int32_t*
 
 // K7: swap gather (pool -> staging) / scatter (staging -> pool).
 void launch_swap_copy(const SwapDesc* ops, const std::int32_t* tok_prefix, int n_ops, int total_tokens,
-                      const KvGeom& g, bf16* stage, bool to_stage, cudaStream_t s);
+                      const KvGeom& g, f16* stage, bool to_stage, cudaStream_t s);
 
 }  // namespace ib2

@@ -4,7 +4,7 @@
 //              parallel attention+MLP residual, one LayerNorm per block
 //   vicuna-13b LLaMA shape: 40 L, d=5120, 40x128 heads, SwiGLU ffn 13824,
 //              RMSNorm, full rotate-half RoPE
-// Weights are bf16, generated on the device from a counter hash (the CPU
+// Weights are f16, generated on the device from a counter hash (the CPU
 // oracle regenerates the identical values); compute accumulates in fp32.
 #pragma once
 
@@ -41,7 +41,7 @@ struct ModelSpec {
 ModelSpec parse_model_json(const std::string& text);
 std::string model_json(const ModelSpec& m);
 
-// Element offsets (bf16 units) of every tensor in the single weight arena.
+// Element offsets (f16 units) of every tensor in the single weight arena.
 struct LayerWeights {
   std::int64_t ln1_g, ln1_b, ln2_g, ln2_b;  // ln2 unused for GPT-J
   std::int64_t w_qkv, b_qkv, w_o, b_o;      // [3D][D], [D][D]

@@ -22,9 +22,9 @@ def run_gemm(a, w, epi, bias=None, resid=None, force_simt=False):
     N = w.shape[0]
     out = outf = None
     if epi in (STORE, GELU):
-        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty(M, N, dtype=torch.float16, device="cuda")
     elif epi == SWIGLU:
-        out = torch.empty(M, N // 2, dtype=torch.bfloat16, device="cuda")
+        out = torch.empty(M, N // 2, dtype=torch.float16, device="cuda")
     elif epi == RESID:
         outf = resid.clone()
     else:
@@ -44,14 +44,14 @@ def reference(a, w, epi, bias=None, resid=None):
     if bias is not None and epi != SWIGLU:
         acc = acc + bias.float()
     if epi == STORE:
-        return acc.bfloat16()
+        return acc.half()
     if epi == GELU:
-        return torch.nn.functional.gelu(acc, approximate="tanh").bfloat16()
+        return torch.nn.functional.gelu(acc, approximate="tanh").half()
     if epi == RESID:
         return resid + acc
     if epi == SWIGLU:
         g, u = acc[:, 0::2], acc[:, 1::2]
-        return (torch.nn.functional.silu(g) * u).bfloat16()
+        return (torch.nn.functional.silu(g) * u).half()
     return acc
 
 
@@ -64,15 +64,15 @@ SHAPES = [(1, 256, 256), (37, 768, 256), (128, 1024, 256), (200, 3072, 1024), (3
 def test_gemm_epilogues(M, N, K, epi):
     import torch
     torch.manual_seed(M * 7 + N + K + epi)
-    a = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
-    w = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
-    bias = (torch.randn(N, device="cuda") * 0.02).bfloat16() if epi != SWIGLU else None
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
+    bias = (torch.randn(N, device="cuda") * 0.02).half() if epi != SWIGLU else None
     resid = torch.randn(M, N, device="cuda") if epi == RESID else None
     got = run_gemm(a, w, epi, bias, resid).float()
     ref = reference(a, w, epi, bias, resid).float()
     scale = ref.abs().max().item() + 1e-6
     err = (got - ref).abs().max().item() / scale
-    tol = 1e-2 if epi in (STORE, GELU, SWIGLU) else 1e-4  # bf16 output rounding vs fp32 outputs
+    tol = 2e-3 if epi in (STORE, GELU, SWIGLU) else 1e-4  # fp16 output rounding vs fp32 outputs
     assert err <= tol, (M, N, K, epi, err)
 
 
@@ -80,8 +80,8 @@ def test_gemm_epilogues(M, N, K, epi):
 def test_tcgen05_matches_simt(M, N, K):
     import torch
     torch.manual_seed(3)
-    a = (torch.randn(M, K, device="cuda") * 0.5).bfloat16()
-    w = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
     x = run_gemm(a, w, STOREF32)
     y = run_gemm(a, w, STOREF32, force_simt=True)
     assert (x - y).abs().max().item() <= 1e-4 * (y.abs().max().item() + 1e-6)
@@ -91,8 +91,8 @@ def test_gemm_bandwidth_smoke():
     # GPT-J QKV at decode batch: weight-bandwidth bound.  Reported, not gated.
     import torch
     M, N, K = 32, 12288, 4096
-    a = (torch.randn(M, K, device="cuda")).bfloat16()
-    w = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+    a = (torch.randn(M, K, device="cuda")).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
     for _ in range(3):
         run_gemm(a, w, STORE)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
