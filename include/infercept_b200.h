@@ -187,10 +187,15 @@ void isim_session_free(isim_session* s);
 /* K3 projection GEMM on caller device pointers: C = A[M][K] . W[N][K]^T with
  * epilogue epi (0 store fp16 (+bias), 1 gelu(acc+bias) fp16, 2 fp32 residual
  * add (+bias), 3 SwiGLU pairs -> fp16 [M][N/2], 4 store fp32 (+bias)).
- * force_simt=1 runs the CUDA-core kernel instead of tcgen05. stream may be 0. */
+ * flags bit 0: run the CUDA-core kernel instead of tcgen05; bit 1: W is
+ * already tile-blocked (isim_debug_tile_weights), else row-major.  Asynchronous
+ * on `stream` (may be 0). */
 isim_status isim_debug_gemm(const void* a, const void* w, int32_t M, int32_t N, int32_t K, int32_t epi,
-                            const void* bias, void* out, int32_t ldo, void* outf, int32_t ldf, int32_t force_simt,
+                            const void* bias, void* out, int32_t ldo, void* outf, int32_t ldf, int32_t flags,
                             void* stream);
+/* Row-major fp16 W[N][K] -> the executor's tile-blocked weight layout
+ * (ceil(N/128)*128*K elements in dst). */
+isim_status isim_debug_tile_weights(const void* src, void* dst, int32_t N, int32_t K, void* stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

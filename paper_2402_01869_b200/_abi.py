@@ -51,7 +51,7 @@ EXPORTS = [
     "isim_exec_create", "isim_exec_step", "isim_exec_sync", "isim_exec_stats_json", "isim_exec_last_tokens",
     "isim_exec_last_logits", "isim_exec_block_table", "isim_exec_free_blocks", "isim_exec_read_kv", "isim_exec_timer", "isim_exec_free",
     "isim_session_open", "isim_session_step", "isim_session_counters", "isim_session_finish", "isim_session_free",
-    "isim_debug_gemm",
+    "isim_debug_gemm", "isim_debug_tile_weights",
 ]
 
 
@@ -105,6 +105,7 @@ def _load():
         "isim_session_finish": (ctypes.c_int, [V, P]),
         "isim_session_free": (None, [V]),
         "isim_debug_gemm": (ctypes.c_int, [V, V, I32, I32, I32, I32, V, V, I32, V, I32, I32, V]),
+        "isim_debug_tile_weights": (ctypes.c_int, [V, V, I32, I32, V]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

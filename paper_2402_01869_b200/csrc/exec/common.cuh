@@ -83,7 +83,7 @@ enum class Epi : int {
 
 struct GemmArgs {
   const f16* a;       // [M][K] row-major (K contiguous)
-  const f16* w;       // [N][K] row-major
+  const f16* w;       // [N][K], tile-blocked (model.hpp weight_tile_offset)
   int M, N, K;
   Epi epi;
   const f16* bias;    // [N] or null

@@ -265,7 +265,9 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
 
   // weights
   weights_ = dalloc<f16>(wl_.total);
-  for (const auto& it : wl_.items) launch_init_tensor(weights_ + it.off, it.count, spec_.weight_seed, it.id, it.kind, main_);
+  for (const auto& it : wl_.items)
+    launch_init_tensor(weights_ + it.off, it.count, spec_.weight_seed, it.id, it.kind, it.rows, it.cols, it.tiled,
+                       main_);
 
   // KV pool and block tables
   const std::int64_t pool_elems = spec_.layers * gpu_blocks_ * 2LL * spec_.d_model * kBlockTokens;

@@ -37,6 +37,7 @@ class B200Executor : public PlanSink {
 
 // Kernel test hook behind isim_debug_gemm (exec/k_gemm_tc.cu).
 void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, const void* bias, void* out, int ldo,
-                void* outf, int ldf, bool force_simt, void* stream);
+                void* outf, int ldf, int flags, void* stream);
+void debug_tile_weights(const void* src, void* dst, int N, int K, void* stream);
 
 }  // namespace ib2

@@ -3,6 +3,7 @@
 // (K not a multiple of 64) and as the in-process cross-check of K3.
 #include "gemm_epilogue.cuh"
 #include "kernels.hpp"
+#include "model.hpp"
 
 namespace ib2 {
 
@@ -21,7 +22,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs a) {
       const int r = i / BK, c = i % BK;
       const int m = m0 + r, n = n0 + r, k = k0 + c;
       sA[c][r] = (m < a.M && k < a.K) ? __half2float(a.a[static_cast<std::int64_t>(m) * a.K + k]) : 0.f;
-      sW[c][r] = (n < a.N && k < a.K) ? __half2float(a.w[static_cast<std::int64_t>(n) * a.K + k]) : 0.f;
+      sW[c][r] = (n < a.N && k < a.K) ? __half2float(a.w[weight_tile_offset(n, k, a.K)]) : 0.f;
     }
     __syncthreads();
 #pragma unroll 8

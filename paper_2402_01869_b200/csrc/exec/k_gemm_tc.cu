@@ -137,7 +137,11 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
         unsigned char* sb = sa + L::A_BYTES;
         mbar_expect_tx(&full[s], L::STAGE_BYTES);
         tma_load_2d(sa, &map_a, &full[s], kb * BK, m0);
-        tma_load_2d(sb, &map_w, &full[s], kb * BK, n0);
+        // Tile-blocked weights: rows of 128-row tile t at k block kb start at
+        // physical row (t * nk + kb) * 128; BN = 256 spans two tiles.
+        const int wt = n0 / 128, wr = n0 % 128;
+        tma_load_2d(sb, &map_w, &full[s], 0, (wt * nk + kb) * 128 + wr);
+        if (BN == 256) tma_load_2d(sb + 128 * BK * 2, &map_w, &full[s], 0, ((wt + 1) * nk + kb) * 128);
       }
     }
   } else if (warp == 1) {
@@ -198,16 +202,22 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
 }
 
 
-// ---- small-M path: swap-AB + deterministic split-K ---------------------------
+// ---- small-M path: swap-AB, persistent whole tiles or cluster K-split ------
 //
-// Decode-dominated iterations have M (tokens) of 8..256 while N x K weights are
-// 17-134 MB per projection: the GEMM is a weight stream.  Computing C^T = W A^T
-// puts 128 weight rows on the UMMA M side (TMEM lanes) and the few tokens on
-// the UMMA N side (NT columns), so every weight byte is read once and the
-// token tile (NT x 64 per stage) is tiny.  Grid = (N/128 weight tiles) x
-// (K splits) sized to ~2 CTAs per SM; each split writes fp32 partials and the
-// last CTA of a tile (atomic ticket) reduces them in split order -- a fixed
-// order, so results are deterministic -- then applies the fused epilogue.
+// Decode-dominated iterations have M (tokens) of 8..256 while the N x K
+// weights are 17-134 MB per projection: the GEMM is a weight stream.  C^T =
+// W A^T puts 128 weight rows on the UMMA M side (TMEM lanes) and the tokens on
+// the UMMA N side (NT columns), so every weight byte is read exactly once.
+//
+// SPLIT == 1 (N/128 >= ~100 tiles: QKV, MLP-in, LM head): persistent, one
+//   CTA per SM owning a contiguous run of whole weight tiles; the TMA ring never
+//   drains between tiles and accumulators alternate between two TMEM buffers so
+//   the epilogue of tile i overlaps the MMAs of tile i+1.
+// SPLIT in {2,4} (few tiles: O and MLP-out, N = d_model): the K range of a
+//   tile is split over a thread-block cluster of SPLIT CTAs; each writes its
+//   fp32 partial tile to its own shared memory and rank 0 sums the partials
+//   over DSMEM (ld.shared::cluster) in rank order -- deterministic, no global
+//   workspace -- before the fused epilogue.
 
 template <int NT, int STAGES>
 struct SkSmem {
@@ -215,8 +225,9 @@ struct SkSmem {
   static constexpr int B_BYTES = NT * BK * 2;  // tokens tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;
-  static constexpr int TMEM_COLS = NT < 32 ? 32 : NT;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
+  static_assert(NT * BM * 4 <= BAR_OFF, "partial tile must fit in the stage ring");
 };
 
 __device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v) {
@@ -230,8 +241,8 @@ __device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v
   }
 }
 
-// Epilogue for one weight row n (this lane) over tokens; SwiGLU pairs come
-// from the neighbouring lane (gate = even row, up = odd row).
+// Epilogue of weight row n (this lane) for token m; SwiGLU pairs come from
+// the neighbouring lane (gate = even row, up = odd row).
 __device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v, int lane) {
   if (a.epi == Epi::SwiGluF16) {
     const float up = __shfl_down_sync(0xffffffffu, v, 1);
@@ -242,24 +253,50 @@ __device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v
   if (m < a.M && n < a.N) epi_one(a, m, n, v);
 }
 
-template <int NT, int STAGES>
+__device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ std::uint32_t tmem_ld16(std::uint32_t taddr, std::uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+  return 0;
+}
+
+template <int NT, int STAGES, int SPLIT>
 __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
-                                                           const __grid_constant__ CUtensorMap map_a, GemmArgs args,
-                                                           float* __restrict__ ws, std::int32_t* __restrict__ tickets) {
+                                                           const __grid_constant__ CUtensorMap map_a, GemmArgs args) {
   using L = SkSmem<NT, STAGES>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + L::BAR_OFF);
   std::uint64_t* empty = full + STAGES;
-  std::uint64_t* done = empty + STAGES;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
-  __shared__ int s_last;
+  std::uint64_t* tfull = empty + STAGES;  // [2] MMA -> epilogue
+  std::uint64_t* tempty = tfull + 2;      // [2] epilogue -> MMA
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BM;
-  const int split = blockIdx.y, splits = gridDim.y;
-  const int nk = args.K / BK;
-  const int kb0 = split * nk / splits, kb1 = (split + 1) * nk / splits;
+  const int tiles = (args.N + BM - 1) / BM, kblocks = args.K / BK;
+  // Segments of this CTA: whole tiles [t0, t1) (SPLIT == 1), or one k range of
+  // one tile (cluster split).
+  int t0, t1, kb0, kb1, rank = 0;
+  if (SPLIT == 1) {
+    t0 = static_cast<int>(static_cast<long long>(blockIdx.x) * tiles / gridDim.x);
+    t1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * tiles / gridDim.x);
+    kb0 = 0;
+    kb1 = kblocks;
+  } else {
+    rank = blockIdx.x % SPLIT;
+    t0 = blockIdx.x / SPLIT;
+    t1 = t0 + 1;
+    kb0 = rank * kblocks / SPLIT;
+    kb1 = (rank + 1) * kblocks / SPLIT;
+  }
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
@@ -268,7 +305,10 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -283,88 +323,108 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int i = kb - kb0, st = i % STAGES;
-        if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
-        unsigned char* sw = smem + st * L::STAGE_BYTES;
-        mbar_expect_tx(&full[st], L::STAGE_BYTES);
-        tma_load_2d(sw, &map_w, &full[st], kb * BK, n0);
-        tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
-      }
+      int i = 0;
+      for (int t = t0; t < t1; ++t)
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          const int st = i % STAGES;
+          if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
+          unsigned char* sw = smem + st * L::STAGE_BYTES;
+          mbar_expect_tx(&full[st], L::STAGE_BYTES);
+          tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
+          tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
+        }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(NT >> 3) << 17) |
                                       (static_cast<std::uint32_t>(BM >> 4) << 24);
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int i = kb - kb0, st = i % STAGES;
-        mbar_wait(&full[st], (i / STAGES) & 1);
+      int i = 0;
+      for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const unsigned char* sw = smem + st * L::STAGE_BYTES;
-        const std::uint64_t da = smem_desc(sw), db = smem_desc(sw + L::A_BYTES);
+        const std::uint32_t acc_tmem = tmem + buf * NT;
+        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+          const int st = i % STAGES;
+          mbar_wait(&full[st], (i / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const unsigned char* sw = smem + st * L::STAGE_BYTES;
+          const std::uint64_t da = smem_desc(sw), db = smem_desc(sw + L::A_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / UMMA_K; ++k) {
-          const std::uint32_t acc = (i > 0 || k > 0) ? 1u : 0u;
-          asm volatile(
-              "{\n"
-              ".reg .pred p;\n"
-              "setp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-              "}\n" ::"r"(tmem),
-              "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const std::uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "setp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+                "}\n" ::"r"(acc_tmem),
+                "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+          }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           su32(&empty[st]))
+                       : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         su32(&empty[st]))
+                         su32(&tfull[buf]))
                      : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(done))
-                   : "memory");
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;
-    const int n = n0 + q * 32 + lane;  // this lane's weight row
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    float* part = ws + (static_cast<std::int64_t>(split) * args.M) * args.N;
+    const int q = warp - 4, row = q * 32 + lane;
+    for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+      const int buf = seg & 1;
+      const int n = t * BM + row;
+      mbar_wait(&tfull[buf], (seg / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      float* part = reinterpret_cast<float*>(smem);  // stage ring is idle once the MMAs completed
 #pragma unroll 1
-    for (int c = 0; c < NT; c += 16) {
-      if (c >= args.M) break;
-      std::uint32_t r[16];
-      const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int c = 0; c < NT; c += 16) {
+        if (c >= args.M) break;
+        std::uint32_t r[16];
+        tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = c + j;
-        const float v = __uint_as_float(r[j]);
-        if (splits == 1) epi_row(args, n, m, v, lane);
-        else if (m < args.M && n < args.N) part[static_cast<std::int64_t>(m) * args.N + n] = v;
-      }
-    }
-    if (splits > 1) {
-      __threadfence();
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (q == 0 && lane == 0) {
-        const int prev = atomicAdd(&tickets[blockIdx.x], 1);
-        s_last = prev == splits - 1;
-        if (s_last) tickets[blockIdx.x] = 0;
-      }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (s_last) {
-        __threadfence();
-        for (int m = 0; m < args.M; ++m) {
-          float v = 0.f;
-          if (n < args.N)
-            for (int sp = 0; sp < splits; ++sp)
-              v += __ldcg(ws + (static_cast<std::int64_t>(sp) * args.M + m) * args.N + n);
-          epi_row(args, n, m, v, lane);
+        for (int j = 0; j < 16; ++j) {
+          const float v = __uint_as_float(r[j]);
+          if (SPLIT == 1) epi_row(args, n, c + j, v, lane);
+          else part[(c + j) * BM + row] = v;
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[buf])) : "memory");
     }
+  }
+  if (SPLIT > 1) {
+    // Partials are in every CTA's shared memory: rank 0 sums them in rank order.
+    cluster_sync_all();
+    if (rank == 0 && warp >= 4) {
+      const int row = (warp - 4) * 32 + lane, n = t0 * BM + row;
+      const std::uint32_t local = su32(smem);
+      std::uint32_t peer[SPLIT];
+#pragma unroll
+      for (int r = 0; r < SPLIT; ++r)
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer[r]) : "r"(local), "r"(r));
+      for (int m0 = 0; m0 < args.M; m0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+#pragma unroll
+        for (int r = 0; r < SPLIT; ++r)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float x = 0.f;
+            if (m0 + j < args.M)
+              asm volatile("ld.shared::cluster.f32 %0, [%1];\n"
+                           : "=f"(x)
+                           : "r"(peer[r] + static_cast<std::uint32_t>(((m0 + j) * BM + row) * 4)));
+            v[j] += x;
+          }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) epi_row(args, n, m0 + j, v[j], lane);
+      }
+    }
+    cluster_sync_all();  // peers' shared memory stays alive until rank 0 is done
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -414,6 +474,9 @@ struct MapKeyHash {
   }
 };
 
+// Tile-blocked weight [N][K] seen by TMA as [ceil(N/128)*128*K/64 rows][64].
+const CUtensorMap& cached_wmap(const void* base, std::int64_t N, int K, int box_rows);
+
 const CUtensorMap& cached_map(const void* base, std::int64_t rows, int K, int box_rows) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
@@ -422,6 +485,11 @@ const CUtensorMap& cached_map(const void* base, std::int64_t rows, int K, int bo
   auto it = cache.find(key);
   if (it == cache.end()) it = cache.emplace(key, make_map(base, rows, K, K, box_rows)).first;
   return it->second;
+}
+
+const CUtensorMap& cached_wmap(const void* base, std::int64_t N, int K, int box_rows) {
+  const std::int64_t phys_rows = (N + 127) / 128 * 128 * (K / BK);
+  return cached_map(base, phys_rows, BK, box_rows);
 }
 
 std::int64_t g_a_rows_capacity = 0;  // rows of every activation buffer (set by the executor)
@@ -436,67 +504,70 @@ void launch_tc(const GemmArgs& a, cudaStream_t s) {
   }
   const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, BM);
-  const CUtensorMap& mw = cached_map(a.w, a.N, a.K, BN);
+  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN == 256 ? 128 : BN);
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
   tc_gemm_kernel<BN, STAGES><<<grid, 256, L::TOTAL, s>>>(ma, mw, a);
   IB2_LAUNCH_CHECK();
 }
 
 
-float* g_ws = nullptr;
-std::int32_t* g_tickets = nullptr;
-std::size_t g_ws_bytes = 0;
-int g_ws_device = -1;
+int g_sms = 0;
 
-template <int NT, int STAGES>
-void launch_skinny(const GemmArgs& a, int splits, cudaStream_t s) {
+template <int NT, int STAGES, int SPLIT>
+void launch_skinny(const GemmArgs& a, int ctas, cudaStream_t s) {
   using L = SkSmem<NT, STAGES>;
   static bool configured = false;
   if (!configured) {
-    IB2_CUDA(cudaFuncSetAttribute(tc_skinny_kernel<NT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    IB2_CUDA(cudaFuncSetAttribute(tc_skinny_kernel<NT, STAGES, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  L::TOTAL));
     configured = true;
   }
   const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
-  const CUtensorMap& mw = cached_map(a.w, a.N, a.K, BM);
+  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
-  tc_skinny_kernel<NT, STAGES><<<dim3((a.N + BM - 1) / BM, splits), 256, L::TOTAL, s>>>(mw, ma, a, g_ws, g_tickets);
-  IB2_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = SPLIT;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_skinny_kernel<NT, STAGES, SPLIT>, mw, ma, a));
 }
 
-// Choose the split so that ~2 CTAs land on every SM, keeping >= 4 K blocks
-// per split, and make sure the fp32 partial workspace is large enough.
-int skinny_splits(const GemmArgs& a) {
-  const int tiles = (a.N + BM - 1) / BM, kblocks = a.K / BK;
-  int sp = (2 * 148 + tiles - 1) / tiles;
-  sp = std::max(1, std::min({sp, kblocks / 4, 16}));
-  const std::size_t need = static_cast<std::size_t>(sp) * a.M * a.N * 4;
-  int dev = 0;
-  IB2_CUDA(cudaGetDevice(&dev));
-  if (sp > 1 && (need > g_ws_bytes || dev != g_ws_device)) {
-    if (g_ws) cudaFree(g_ws);
-    if (!g_tickets || dev != g_ws_device) {
-      IB2_CUDA(cudaMalloc(&g_tickets, 65536 * 4));
-      IB2_CUDA(cudaMemset(g_tickets, 0, 65536 * 4));
-    }
-    g_ws_bytes = std::max<std::size_t>(need, 64u << 20);
-    IB2_CUDA(cudaMalloc(&g_ws, g_ws_bytes));
-    g_ws_device = dev;
-  }
-  return sp;
+template <int NT, int STAGES>
+void launch_skinny_nt(const GemmArgs& a, cudaStream_t s) {
+  const int tiles = static_cast<int>((a.N + BM - 1) / BM), kblocks = a.K / BK;
+  // Enough weight tiles (>= 2/3 of the SMs): persistent whole tiles.  Few
+  // tiles: split K over a cluster of 4/3/2 CTAs per tile, one wave.
+  if (tiles * 3 >= g_sms * 2 || kblocks < 16) launch_skinny<NT, STAGES, 1>(a, std::min(g_sms, tiles), s);
+  else if (tiles * 4 <= g_sms) launch_skinny<NT, STAGES, 4>(a, tiles * 4, s);
+  else if (tiles * 3 <= g_sms) launch_skinny<NT, STAGES, 3>(a, tiles * 3, s);
+  else if (tiles * 2 <= g_sms) launch_skinny<NT, STAGES, 2>(a, tiles * 2, s);
+  else launch_skinny<NT, STAGES, 1>(a, std::min(g_sms, tiles), s);
 }
 
 bool skinny_ok(const GemmArgs& a) {
   static const bool off = getenv("IB2_NO_SKINNY") != nullptr;
-  return !off && a.M <= 256 && a.K % BK == 0 && a.N % 2 == 0 && (a.N + BM - 1) / BM <= 65536;
+  return !off && a.M <= 256 && a.K % BK == 0 && a.N % 2 == 0;
 }
 
 void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
-  const int sp = skinny_splits(a);
-  if (a.M <= 16) launch_skinny<16, 8>(a, sp, s);
-  else if (a.M <= 32) launch_skinny<32, 8>(a, sp, s);
-  else if (a.M <= 64) launch_skinny<64, 8>(a, sp, s);
-  else if (a.M <= 128) launch_skinny<128, 6>(a, sp, s);
-  else launch_skinny<256, 4>(a, sp, s);
+  if (!g_sms) {
+    int dev = 0;
+    IB2_CUDA(cudaGetDevice(&dev));
+    IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (a.M <= 16) launch_skinny_nt<16, 10>(a, s);
+  else if (a.M <= 32) launch_skinny_nt<32, 9>(a, s);
+  else if (a.M <= 64) launch_skinny_nt<64, 8>(a, s);
+  else if (a.M <= 128) launch_skinny_nt<128, 6>(a, s);
+  else launch_skinny_nt<256, 4>(a, s);
 }
 
 }  // namespace
@@ -523,8 +594,27 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s) {
   else launch_tc<64, 8>(a, s);
 }
 
+void debug_tile_weights(const void* src, void* dst, int N, int K, void* stream) {
+  if (K % BK) throw DeviceError("debug_tile_weights: K must be a multiple of 64");
+  launch_tile_weights(static_cast<const f16*>(src), static_cast<f16*>(dst), N, K, static_cast<cudaStream_t>(stream));
+}
+
 void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, const void* bias, void* out, int ldo,
-                void* outf, int ldf, bool force_simt, void* stream) {
+                void* outf, int ldf, int flags, void* stream) {
+  const bool force_simt = flags & 1;
+  if (!(flags & 2)) {
+  // The executor keeps weights tile-blocked; the hook takes row-major W.
+  static f16* tiled = nullptr;
+  static std::size_t tiled_elems = 0;
+  const std::size_t need = static_cast<std::size_t>((N + 127) / 128 * 128) * K;
+  if (need > tiled_elems) {
+    if (tiled) cudaFree(tiled);
+    IB2_CUDA(cudaMalloc(&tiled, need * sizeof(f16)));
+    tiled_elems = need;
+  }
+  launch_tile_weights(static_cast<const f16*>(w), tiled, N, K, static_cast<cudaStream_t>(stream));
+  w = tiled;
+  }
   GemmArgs g{static_cast<const f16*>(a), static_cast<const f16*>(w), M, N, K, static_cast<Epi>(epi),
              static_cast<const f16*>(bias), static_cast<f16*>(out), ldo, static_cast<float*>(outf), ldf};
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -533,7 +623,6 @@ void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, cons
   if (force_simt) launch_gemm_simt(g, s);
   else launch_gemm(g, s);
   g_a_rows_capacity = saved;
-  IB2_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace ib2

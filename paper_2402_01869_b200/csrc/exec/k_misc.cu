@@ -29,11 +29,36 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
   return t;
 }
 
-__global__ void init_tensor_kernel(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind) {
+// Values depend on the LOGICAL index only; tiled weights store logical
+// (n, k) at its tile-blocked offset, padding rows are zero.
+__global__ void init_tensor_kernel(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
+                                   std::int64_t rows, std::int64_t cols, int tiled) {
+  const std::int64_t kb = cols / 64;
   for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
-    float v = kind == 1 ? 1.0f : (kind == 2 ? 0.0f : synth_weight(seed, id, static_cast<std::uint64_t>(i)));
+    std::int64_t logical = i;
+    bool pad = false;
+    if (tiled) {
+      const std::int64_t tile = i / 8192, rem = i % 8192;
+      const std::int64_t n = (tile / kb) * 128 + rem / 64, k = (tile % kb) * 64 + rem % 64;
+      pad = n >= rows;
+      logical = n * cols + k;
+    }
+    const float v = pad ? 0.0f
+                        : (kind == 1 ? 1.0f : (kind == 2 ? 0.0f : synth_weight(seed, id, static_cast<std::uint64_t>(logical))));
     dst[i] = __float2half_rn(v);
+  }
+}
+
+// Row-major [N][K] -> tile-blocked (for the kernel test hook).
+__global__ void tile_weights_kernel(const f16* __restrict__ src, f16* __restrict__ dst, std::int64_t N, std::int64_t K,
+                                    std::int64_t count) {
+  const std::int64_t kb = K / 64;
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t tile = i / 8192, rem = i % 8192;
+    const std::int64_t n = (tile / kb) * 128 + rem / 64, k = (tile % kb) * 64 + rem % 64;
+    dst[i] = n < N ? src[n * K + k] : __float2half_rn(0.f);
   }
 }
 
@@ -281,8 +306,14 @@ int grid_for(std::int64_t n, int threads) {
 }  // namespace
 
 void launch_init_tensor(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
-                        cudaStream_t s) {
-  init_tensor_kernel<<<grid_for(count, 256), 256, 0, s>>>(dst, count, seed, id, kind);
+                        std::int64_t rows, std::int64_t cols, bool tiled, cudaStream_t s) {
+  init_tensor_kernel<<<grid_for(count, 256), 256, 0, s>>>(dst, count, seed, id, kind, rows, cols, tiled ? 1 : 0);
+  IB2_LAUNCH_CHECK();
+}
+
+void launch_tile_weights(const f16* src, f16* dst, std::int64_t N, std::int64_t K, cudaStream_t s) {
+  const std::int64_t count = (N + 127) / 128 * 128 * K;
+  tile_weights_kernel<<<grid_for(count, 256), 256, 0, s>>>(src, dst, N, K, count);
   IB2_LAUNCH_CHECK();
 }
 

@@ -20,7 +20,8 @@ struct KvGeom {
 
 // init
 void launch_init_tensor(f16* dst, std::int64_t count, std::uint64_t seed, std::uint32_t id, int kind,
-                        cudaStream_t s);
+                        std::int64_t rows, std::int64_t cols, bool tiled, cudaStream_t s);
+void launch_tile_weights(const f16* src, f16* dst, std::int64_t N, std::int64_t K, cudaStream_t s);
 void launch_iota_desc(std::int32_t* stack, std::int64_t n, cudaStream_t s);
 void launch_fill_i32(std::int32_t* p, std::int64_t n, std::int32_t v, cudaStream_t s);
 

@@ -107,6 +107,17 @@ WeightLayout layout_weights(const ModelSpec& m) {
     w.total += (count + 63) / 64 * 64;
     return off;
   };
+  // Projection weight [N][K], tile-blocked (weight_tile_offset).
+  auto put_w = [&](std::int64_t N, std::int64_t K) {
+    const std::int64_t off = w.total;
+    WeightLayout::Item it{off, tiled_weight_elems(N, K), next_id++, 0};
+    it.rows = N;
+    it.cols = K;
+    it.tiled = true;
+    w.items.push_back(it);
+    w.total += it.count;
+    return off;
+  };
   const bool bias = m.has_bias();
   w.tok_emb = put(V * D, 0);
   if (m.family == Family::Gpt2) w.pos_emb = put(static_cast<std::int64_t>(m.max_pos) * D, 0);
@@ -120,19 +131,19 @@ WeightLayout layout_weights(const ModelSpec& m) {
     } else {
       L.ln2_g = L.ln2_b = -1;
     }
-    L.w_qkv = put(3 * D * D, 0);
+    L.w_qkv = put_w(3 * D, D);
     L.b_qkv = m.qkv_bias() ? put(3 * D, 0) : -1;
-    L.w_o = put(D * D, 0);
+    L.w_o = put_w(D, D);
     L.b_o = m.family == Family::Gpt2 ? put(D, 0) : -1;
-    L.w_in = put(static_cast<std::int64_t>(m.ffn_in_width()) * D, 0);
+    L.w_in = put_w(m.ffn_in_width(), D);
     L.b_in = bias ? put(F, 0) : -1;
-    L.w_out = put(D * F, 0);
+    L.w_out = put_w(D, F);
     L.b_out = bias ? put(D, 0) : -1;
     w.layer.push_back(L);
   }
   w.lnf_g = put(D, 1);
   w.lnf_b = bias ? put(D, 2) : -1;
-  w.lm_w = put(V * D, 0);
+  w.lm_w = put_w(V, D);
   w.lm_b = m.lm_bias() ? put(V, 0) : -1;
   return w;
 }

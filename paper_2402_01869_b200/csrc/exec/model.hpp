@@ -53,14 +53,35 @@ struct WeightLayout {
   std::int64_t lnf_g = 0, lnf_b = 0, lm_w = 0, lm_b = -1;  // [V][D]
   std::int64_t total = 0;
   // (offset, count, tensor id, kind) for the device initializer; kind:
-  // 0 = uniform(std 0.02), 1 = ones, 2 = zeros.
+  // 0 = uniform(std 0.02), 1 = ones, 2 = zeros.  Projection weights [N][K]
+  // are stored tile-blocked (tiled = true, see weight_tile_offset): every
+  // 128-row x 64-column tile is one contiguous 16 KB run, so a TMA load of a
+  // tile streams contiguous HBM.  N is padded to a multiple of 128 (zeros).
   struct Item {
     std::int64_t off, count;
     std::uint32_t id;
     int kind;
+    std::int64_t rows = 0, cols = 0;
+    bool tiled = false;
   };
   std::vector<Item> items;
 };
 WeightLayout layout_weights(const ModelSpec& m);
+
+#ifdef __CUDACC__
+#define IB2_HD __host__ __device__
+#else
+#define IB2_HD
+#endif
+
+// Element offset of logical (n, k) in a tile-blocked [N][K] weight.
+constexpr int kWTileRows = 128, kWTileCols = 64;
+IB2_HD inline std::int64_t weight_tile_offset(std::int64_t n, std::int64_t k, std::int64_t K) {
+  return ((n / kWTileRows) * (K / kWTileCols) + k / kWTileCols) * (kWTileRows * kWTileCols) +
+         (n % kWTileRows) * kWTileCols + k % kWTileCols;
+}
+inline std::int64_t tiled_weight_elems(std::int64_t N, std::int64_t K) {
+  return (N + kWTileRows - 1) / kWTileRows * kWTileRows * K;
+}
 
 }  // namespace ib2
