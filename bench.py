@@ -105,8 +105,8 @@ def shard_trace(ib, world, rank, tmpdir):
     return ib.Trace.load(out)
 
 
-def gpu_pools(host_gb):
-    blocks = int(COST["gpu_kv_capacity"] // (16 * GPTJ_M)) + 512
+def gpu_pools(host_gb, gpu_blocks=0):
+    blocks = gpu_blocks or int(COST["gpu_kv_capacity"] // (16 * GPTJ_M)) + 512
     return dict(gpu_blocks=blocks, host_bytes=int(host_gb * 1e9), max_requests=1024, max_rows=4096, timing=True,
                 stage_tokens=3328)
 
@@ -149,7 +149,7 @@ def run_b200(args):
     tmp = tempfile.mkdtemp()
     trace = shard_trace(ib, world, rank, tmp)
     cost = ib.CostModel.from_json(COST)
-    ex = ib.Executor({"preset": "gptj-6b"}, local, gpu_pools(args.host_gb))
+    ex = ib.Executor({"preset": "gptj-6b"}, local, gpu_pools(args.host_gb, args.gpu_blocks))
     sess = ib.Session(trace, cost, {"policy": "infercept", "estimator": "oracle"}, ex)
 
     # Fast-forward to steady state, then warm up.
@@ -321,6 +321,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--host-gb", type=float, default=48.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gpu-blocks", type=int, default=0,
+                    help="override the KV pool size (profiling runs only; the scheduler's capacity is unchanged)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

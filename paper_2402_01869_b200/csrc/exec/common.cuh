@@ -4,6 +4,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <string>
+#include <utility>
 
 #include "../sched/base.hpp"
 
@@ -21,6 +23,29 @@ using f16 = __half;  // activations, KV cache and weights; fp32 accumulation
 #define IB2_LAUNCH_CHECK() IB2_CUDA(cudaGetLastError())
 
 constexpr int kBlockTokens = 16;  // paged KV block = 16 token positions
+
+// Programmatic dependent launch: every per-iteration kernel lets its successor
+// launch immediately (its prologue overlaps this kernel's tail) and waits for
+// its predecessor's completion before touching global memory it produced.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  if (e != cudaSuccess) throw DeviceError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
 
 // splitmix64 finalizer: the counter hash behind synthetic weights and ids.
 __host__ __device__ inline std::uint64_t mix64(std::uint64_t z) {
@@ -55,13 +80,25 @@ struct RowDesc {
   std::int64_t req_id;
 };
 
-// A tile of consecutive chunk rows of one request for prefill attention.
+// A tile of consecutive chunk rows of one request for prefill attention,
+// restricted to keys [kv_lo, kv_hi) (split-KV).  part < 0: the item covers
+// all keys and writes the normalized output; else it writes an fp32 partial
+// (o, m, l) into slot `part` for the combine pass.
 struct TileDesc {
   std::int32_t row0;   // first batch row
   std::int32_t nrows;  // <= 64
   std::int32_t slot;
   std::int32_t pos0;   // position of row0
+  std::int32_t kv_lo, kv_hi;
+  std::int32_t part;
+  std::int32_t pad;
 };
+
+// Split q-tiles whose partials must be merged.
+struct CombineDesc {
+  std::int32_t row0, nrows, part0, nparts;
+};
+constexpr int kMaxChunkParts = 640;  // (part, head) slots of the split-KV workspace
 
 // Swap copy descriptor: positions [pos0, pos0+n) of a slot <-> staging rows.
 struct SwapDesc {

@@ -15,6 +15,7 @@
 // Swap copies are asynchronous cudaMemcpyAsync on a dedicated copy stream;
 // staging buffers are double-buffered and ordered with events.
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -42,7 +43,8 @@ class HostArena {
     cap_ = bytes;
     used_ = 0;
   }
-  std::size_t alloc(std::size_t n) {
+  static constexpr std::size_t kNone = ~std::size_t(0);
+  std::size_t try_alloc(std::size_t n) {
     n = (n + 255) & ~std::size_t(255);
     for (auto it = free_.begin(); it != free_.end(); ++it) {
       if (it->second >= n) {
@@ -53,9 +55,9 @@ class HostArena {
         return off;
       }
     }
-    throw DeviceError("pinned host swap pool exhausted (" + std::to_string(used_) + " of " + std::to_string(cap_) +
-                      " bytes in use)");
+    return kNone;
   }
+  std::string describe() const { return std::to_string(used_) + " of " + std::to_string(cap_) + " bytes in use"; }
   void release(std::size_t off, std::size_t n) {
     n = (n + 255) & ~std::size_t(255);
     used_ -= n;
@@ -87,6 +89,7 @@ struct Extent {
   std::int64_t lo, hi;    // positions still resident on the host
   std::size_t off;        // arena offset
   std::size_t bytes;
+  std::int64_t d2h_seq;   // 1-based index of the D2H batch that wrote it
 };
 
 template <typename T>
@@ -130,9 +133,27 @@ class Impl final : public B200Executor {
   ModelSpec spec_;
   WeightLayout wl_;
   int dev_ = 0;
-  cudaStream_t main_ = nullptr, copy_ = nullptr;
+  // copy_ carries D2H (swap-out), copy_in_ H2D (swap-in): PCIe is full duplex.
+  cudaStream_t main_ = nullptr, copy_ = nullptr, copy_in_ = nullptr;
+  static constexpr int kSeqRing = 64;
+  cudaEvent_t d2h_ring_[kSeqRing] = {}, h2d_ring_[kSeqRing] = {};
+  std::int64_t d2h_seq_ = 0, h2d_seq_ = 0;
+  struct PendingRelease {
+    std::size_t off, bytes;
+    std::int64_t h2d_seq;  // host memory reusable once this many H2D batches completed
+  };
+  std::vector<PendingRelease> pending_release_;
+  void release_extent_memory(std::size_t off, std::size_t bytes) { pending_release_.push_back({off, bytes, h2d_seq_}); }
+  void retire_host_memory(bool force);
+  std::size_t host_alloc(std::size_t bytes);
   bool record_ = false, timing_ = false;
   bool force_row_attention_ = false;  // diagnostics: every row through K1
+  // diagnostics: per-iteration start events on the compute stream + the
+  // iteration's composition (rows, decode rows, chunk rows, swap-in, swap-out)
+  bool trace_iters_ = false;
+  std::vector<cudaEvent_t> iter_ev_;
+  std::vector<std::array<std::int64_t, 5>> iter_info_;
+  std::vector<double> iter_ms_;
 
   f16* weights_ = nullptr;
   std::int64_t gpu_blocks_ = 0;
@@ -173,14 +194,18 @@ class Impl final : public B200Executor {
   };
   struct PendingIn {
     int buf, n_ops, tokens;
+    std::vector<std::int64_t> requests;  // whose blocks the scatter fills
   };
+  static constexpr int kSwapBufs = 3;
   static constexpr int kMaxSwapOps = 4096;
-  SwapBuf in_[2], out_[2];
+  SwapBuf in_[kSwapBufs], out_[kSwapBufs];
   int in_next_ = 0, out_next_ = 0;
   std::vector<PendingIn> pending_in_;
   std::int64_t stage_tokens_ = 0;
   bool overlap_swaps_ = true;
-  void flush_swap_ins();
+  void flush_swap_ins();                       // all pending scatters
+  void flush_swap_ins_for(const isim_batch_plan& p);  // those the plan touches
+  void flush_swap_in_buffer(int buf);
   double swap_ms_ = 0.0;
   double swap_bytes_timed_ = 0.0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> swap_ev_pending_;
@@ -216,6 +241,9 @@ class Impl final : public B200Executor {
   const RowDesc* rows_dev_ = nullptr;
   const std::int32_t* drows_dev_ = nullptr;
   const TileDesc* tiles_dev_ = nullptr;
+  const CombineDesc* combines_dev_ = nullptr;
+  int n_combines_ = 0;
+  float *chunk_ws_o_ = nullptr, *chunk_ws_ml_ = nullptr;
   const std::int32_t* samples_dev_ = nullptr;
   double k1_bytes_iter_ = 0.0;
   int max_pos1_ = 0;
@@ -235,9 +263,15 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   if (prop.major != 10) throw DeviceError(std::string("executor is built for sm_100a; device is ") + prop.name);
   IB2_CUDA(cudaStreamCreateWithFlags(&main_, cudaStreamNonBlocking));
   IB2_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+  IB2_CUDA(cudaStreamCreateWithFlags(&copy_in_, cudaStreamNonBlocking));
+  for (int i = 0; i < kSeqRing; ++i) {
+    IB2_CUDA(cudaEventCreateWithFlags(&d2h_ring_[i], cudaEventDisableTiming));
+    IB2_CUDA(cudaEventCreateWithFlags(&h2d_ring_[i], cudaEventDisableTiming));
+  }
   record_ = pj.value("record", false);
   timing_ = pj.value("timing", false);
   force_row_attention_ = pj.value("row_attention", false);
+  trace_iters_ = pj.value("trace_iterations", false);
 
   max_slots_ = pj.value("max_requests", 1024);
   max_rows_ = pj.value("max_rows", 4096);
@@ -318,9 +352,12 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   part_o_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * spec_.head_dim());
   part_ml_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * 2);
   set_gemm_activation_rows(max_rows_);
+  chunk_ws_o_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * 64 * spec_.head_dim());
+  chunk_ws_ml_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * 64 * 2);
 
   // plan ring
-  plan_bytes_ = static_cast<std::size_t>(max_rows_) * (sizeof(RowDesc) + 4 * 4 + sizeof(TileDesc)) +
+  plan_bytes_ = static_cast<std::size_t>(max_rows_) * (sizeof(RowDesc) + 4 * 4) +
+                static_cast<std::size_t>(kMaxChunkParts + max_rows_) * (sizeof(TileDesc) + sizeof(CombineDesc)) +
                 static_cast<std::size_t>(max_slots_) * max_lb_ * 4 * 3 + 4096;
   for (int i = 0; i < kRing; ++i) {
     IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[i]), plan_bytes_, cudaHostAllocDefault));
@@ -335,7 +372,7 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   // swap path
   IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_bytes_, cudaHostAllocDefault));
   arena_.reset(host_bytes_);
-  for (SwapBuf* b : {&in_[0], &in_[1], &out_[0], &out_[1]}) {
+  for (SwapBuf* b : {&in_[0], &in_[1], &in_[2], &out_[0], &out_[1], &out_[2]}) {
     b->stage = dalloc<f16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
     b->desc_dev = dalloc<SwapDesc>(kMaxSwapOps);
     b->prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 1);
@@ -367,7 +404,7 @@ Impl::~Impl() {
   cudaEventDestroy(mark_[0]);
   cudaEventDestroy(mark_[1]);
   cudaFreeHost(host_pool_);
-  for (SwapBuf* b : {&in_[0], &in_[1], &out_[0], &out_[1]}) {
+  for (SwapBuf* b : {&in_[0], &in_[1], &in_[2], &out_[0], &out_[1], &out_[2]}) {
     cudaFree(b->stage);
     cudaFree(b->desc_dev);
     cudaFree(b->prefix_dev);
@@ -377,11 +414,16 @@ Impl::~Impl() {
     cudaEventDestroy(b->consumed);
   }
   void* ptrs[] = {weights_, pool_, table_, stack_, top_, err_, hist_, rope_cs_, x_, xn_, qkv_, attn_, hid_, lmrows_,
-                  logits_, out_tok_, part_o_, part_ml_};
+                  logits_, out_tok_, part_o_, part_ml_, chunk_ws_o_, chunk_ws_ml_};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   cudaStreamDestroy(main_);
   cudaStreamDestroy(copy_);
+  cudaStreamDestroy(copy_in_);
+  for (int i = 0; i < kSeqRing; ++i) {
+    cudaEventDestroy(d2h_ring_[i]);
+    cudaEventDestroy(h2d_ring_[i]);
+  }
 }
 
 int Impl::slot_for(std::int64_t rid) {
@@ -462,17 +504,68 @@ void Impl::apply_ops(const isim_batch_plan& p, int phase, std::vector<std::int32
   }
 }
 
-void Impl::flush_swap_ins() {
-  for (const PendingIn& p : pending_in_) {
+void Impl::retire_host_memory(bool force) {
+  if (force) IB2_CUDA(cudaStreamSynchronize(copy_in_));
+  std::size_t keep = 0;
+  for (std::size_t i = 0; i < pending_release_.size(); ++i) {
+    const PendingRelease& r = pending_release_[i];
+    bool done = force || r.h2d_seq == 0;
+    if (!done) {
+      const cudaError_t q = cudaEventQuery(h2d_ring_[(r.h2d_seq - 1) % kSeqRing]);
+      if (q != cudaSuccess && q != cudaErrorNotReady) IB2_CUDA(q);
+      done = q == cudaSuccess;
+    }
+    if (done) arena_.release(r.off, r.bytes);
+    else pending_release_[keep++] = r;
+  }
+  pending_release_.resize(keep);
+}
+
+std::size_t Impl::host_alloc(std::size_t bytes) {
+  std::size_t off = arena_.try_alloc(bytes);
+  if (off == HostArena::kNone) {
+    retire_host_memory(true);
+    off = arena_.try_alloc(bytes);
+  }
+  if (off == HostArena::kNone) throw DeviceError("pinned host swap pool exhausted (" + arena_.describe() + ")");
+  return off;
+}
+
+// Swap-in scatters are issued lazily: the H2D of a batch overlaps later
+// iterations until the restored request is touched by a plan (rows or ops),
+// its staging buffer is recycled, or the executor synchronizes.
+void Impl::flush_swap_in_buffer(int buf) {
+  for (std::size_t i = 0; i < pending_in_.size(); ++i) {
+    if (pending_in_[i].buf != buf) continue;
+    const PendingIn p = pending_in_[i];
+    pending_in_.erase(pending_in_.begin() + static_cast<std::ptrdiff_t>(i));
     SwapBuf& b = in_[p.buf];
-    IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));
-    IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, p.n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
-    IB2_CUDA(cudaMemcpyAsync(b.prefix_dev, b.prefix_host, (p.n_ops + 1) * 4, cudaMemcpyHostToDevice, main_));
+    IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));  // descriptors + data landed (copy_in_)
     launch_swap_copy(b.desc_dev, b.prefix_dev, p.n_ops, p.tokens, geom(), b.stage, false, main_);
     ++kernel_launches_;
     IB2_CUDA(cudaEventRecord(b.consumed, main_));
+    return;
   }
-  pending_in_.clear();
+}
+
+void Impl::flush_swap_ins() {
+  while (!pending_in_.empty()) flush_swap_in_buffer(pending_in_.front().buf);
+}
+
+void Impl::flush_swap_ins_for(const isim_batch_plan& p) {
+  if (pending_in_.empty()) return;
+  std::vector<int> bufs;
+  auto touched = [&](std::int64_t rid) {
+    for (const PendingIn& q : pending_in_)
+      if (std::find(q.requests.begin(), q.requests.end(), rid) != q.requests.end()) bufs.push_back(q.buf);
+  };
+  for (int i = 0; i < p.n_ops; ++i) touched(p.ops[i].request_id);
+  for (int i = 0; i < p.n_spans; ++i) touched(p.spans[i].request_id);
+  // Flush in issue order (a request may have batches in several buffers).
+  for (std::size_t i = 0; i < pending_in_.size();) {
+    if (std::find(bufs.begin(), bufs.end(), pending_in_[i].buf) != bufs.end()) flush_swap_in_buffer(pending_in_[i].buf);
+    else ++i;
+  }
 }
 
 void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std::int64_t>& req_of, bool swap_in) {
@@ -515,11 +608,13 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     const int n_ops = static_cast<int>(last - first);
     SwapBuf& b = swap_in ? in_[in_next_] : out_[out_next_];
     const int bi = swap_in ? in_next_ : out_next_;
-    if (swap_in) in_next_ ^= 1;
-    else out_next_ ^= 1;
-    // The pinned descriptor arrays of this buffer were last uploaded two uses
-    // ago; make sure that upload (and the kernel reading them) is done.
-    IB2_CUDA(cudaEventSynchronize(b.consumed));
+    if (swap_in) in_next_ = (in_next_ + 1) % kSwapBufs;
+    else out_next_ = (out_next_ + 1) % kSwapBufs;
+    if (swap_in) flush_swap_in_buffer(bi);  // recycle: its previous batch must be scattered first
+    // The pinned descriptor arrays of this buffer were last uploaded
+    // kSwapBufs uses ago (swap-in: on copy_in_ before that batch's data;
+    // swap-out: on the compute stream before its gather).
+    IB2_CUDA(cudaEventSynchronize(swap_in ? b.copied : b.consumed));
     std::int64_t off = 0;
     b.prefix_host[0] = 0;
     for (int k = 0; k < n_ops; ++k) {
@@ -536,8 +631,14 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     }
     const double batch_bytes = static_cast<double>(tokens) * static_cast<double>(L) * static_cast<double>(row_bytes);
     if (swap_in) {
-      IB2_CUDA(cudaStreamWaitEvent(copy_, b.consumed, 0));  // staging free again
-      if (t0) IB2_CUDA(cudaEventRecord(t0, copy_));
+      IB2_CUDA(cudaStreamWaitEvent(copy_in_, b.consumed, 0));  // staging + descriptors free again
+      IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, copy_in_));
+      IB2_CUDA(cudaMemcpyAsync(b.prefix_dev, b.prefix_host, (n_ops + 1) * 4, cudaMemcpyHostToDevice, copy_in_));
+      std::int64_t need_d2h = 0;  // extents must have landed on the host
+      for (int k = 0; k < n_ops; ++k)
+        need_d2h = std::max(need_d2h, extents_[ext_of[first + k].first][ext_of[first + k].second].d2h_seq);
+      if (need_d2h > 0) IB2_CUDA(cudaStreamWaitEvent(copy_in_, d2h_ring_[(need_d2h - 1) % kSeqRing], 0));
+      if (t0) IB2_CUDA(cudaEventRecord(t0, copy_in_));
       for (int k = 0; k < n_ops; ++k) {
         const Extent& x = extents_[ext_of[first + k].first][ext_of[first + k].second];
         const std::int64_t n0 = x.hi0 - x.lo0;
@@ -545,18 +646,23 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
         IB2_CUDA(cudaMemcpy2DAsync(b.stage + b.desc_host[k].stage_off, static_cast<std::size_t>(b.desc_host[k].n) * row_bytes,
                                    src, static_cast<std::size_t>(n0) * row_bytes,
                                    static_cast<std::size_t>(b.desc_host[k].n) * row_bytes, L, cudaMemcpyHostToDevice,
-                                   copy_));
+                                   copy_in_));
         extents_[ext_of[first + k].first][ext_of[first + k].second].lo = b.desc_host[k].pos0 + b.desc_host[k].n;
       }
-      IB2_CUDA(cudaEventRecord(b.copied, copy_));
+      IB2_CUDA(cudaEventRecord(b.copied, copy_in_));
+      IB2_CUDA(cudaEventRecord(h2d_ring_[h2d_seq_ % kSeqRing], copy_in_));
+      ++h2d_seq_;
       if (t1) {
-        IB2_CUDA(cudaEventRecord(t1, copy_));
+        IB2_CUDA(cudaEventRecord(t1, copy_in_));
         swap_ev_pending_.push_back({t0, t1});
         swap_ev_bytes_.push_back(batch_bytes);
       }
-      pending_in_.push_back({bi, n_ops, tokens});
-      // Only the final batch of an iteration may stay in flight.
-      if (last < ops.size() || !overlap_swaps_) flush_swap_ins();
+      std::vector<std::int64_t> reqs;
+      for (int k = 0; k < n_ops; ++k)
+        if (std::find(reqs.begin(), reqs.end(), ext_of[first + k].first) == reqs.end())
+          reqs.push_back(ext_of[first + k].first);
+      pending_in_.push_back({bi, n_ops, tokens, std::move(reqs)});
+      if (!overlap_swaps_) flush_swap_ins();
     } else {
       IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));  // previous D2H out of this staging done
       IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
@@ -568,14 +674,16 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
       if (t0) IB2_CUDA(cudaEventRecord(t0, copy_));
       for (int k = 0; k < n_ops; ++k) {
         const std::size_t bytes = static_cast<std::size_t>(b.desc_host[k].n) * L * row_bytes;
-        const std::size_t hoff = arena_.alloc(bytes);
+        const std::size_t hoff = host_alloc(bytes);
         IB2_CUDA(cudaMemcpyAsync(host_pool_ + hoff, b.stage + b.desc_host[k].stage_off, bytes, cudaMemcpyDeviceToHost,
                                  copy_));
         extents_[ext_of[first + k].first].push_back({b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n,
                                                      b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n, hoff,
-                                                     bytes});
+                                                     bytes, d2h_seq_ + 1});
       }
       IB2_CUDA(cudaEventRecord(b.copied, copy_));
+      IB2_CUDA(cudaEventRecord(d2h_ring_[d2h_seq_ % kSeqRing], copy_));
+      ++d2h_seq_;
       if (t1) {
         IB2_CUDA(cudaEventRecord(t1, copy_));
         swap_ev_pending_.push_back({t0, t1});
@@ -586,14 +694,14 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     first = last;
   }
   if (swap_in) {
-    // Fully consumed extents go back to the arena; later D2H copies into that
-    // memory are queued behind these H2D reads on the same copy stream.
+    // Fully consumed extents return to the arena once the H2D copies reading
+    // them have completed (the D2H stream may otherwise overwrite them).
     for (const auto& [rid, idx] : ext_of) {
       (void)idx;
       auto& exts = extents_[rid];
       for (std::size_t e = 0; e < exts.size();) {
         if (exts[e].lo >= exts[e].hi) {
-          arena_.release(exts[e].off, exts[e].bytes);
+          release_extent_memory(exts[e].off, exts[e].bytes);
           exts.erase(exts.begin() + static_cast<std::ptrdiff_t>(e));
         } else {
           ++e;
@@ -605,6 +713,13 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
 
 void Impl::consume(const isim_batch_plan& p) {
   IB2_CUDA(cudaSetDevice(dev_));
+  retire_host_memory(false);
+  if (trace_iters_) {
+    cudaEvent_t e;
+    IB2_CUDA(cudaEventCreate(&e));
+    IB2_CUDA(cudaEventRecord(e, main_));
+    iter_ev_.push_back(e);
+  }
   const int D = spec_.d_model;
 
   // ---- host-side plan lowering ------------------------------------------------
@@ -626,12 +741,47 @@ void Impl::consume(const isim_batch_plan& p) {
     if (sp.count == 1 || force_row_attention_) {
       for (int k = 0; k < sp.count; ++k) drows.push_back(r0 + k);
     } else {
-      for (int k = 0; k < sp.count; k += 64) tiles.push_back({r0 + k, std::min(64, sp.count - k), slot, sp.pos + k});
+      for (int k = 0; k < sp.count; k += 64)
+        tiles.push_back({r0 + k, std::min(64, sp.count - k), slot, sp.pos + k, 0, 0, -1, 0});
     }
     if (sp.sample) samples.push_back(r0 + sp.count - 1);
   }
   const int n_rows = static_cast<int>(rows.size());
   if (n_rows > max_rows_) throw DeviceError("executor: batch exceeds max_rows");
+  // Split-KV for chunk tiles: aim for ~2 waves of (item, head) CTAs; a tile's
+  // keys are split into 64-aligned ranges of >= 256 keys.
+  std::vector<TileDesc> items;
+  std::vector<CombineDesc> combines;
+  {
+    const int H = spec_.heads;
+    const int base_ctas = static_cast<int>(tiles.size()) * H;
+    const int want = base_ctas > 0 ? std::max(1, (2 * 148 + base_ctas - 1) / base_ctas) : 1;
+    int parts = 0;
+    for (const TileDesc& t : tiles) {
+      const int keys = t.pos0 + t.nrows;
+      int sp = std::min(want, std::max(1, keys / 256));
+      if ((parts + sp) * H > kMaxChunkParts) sp = 1;
+      if (sp == 1) {
+        TileDesc w = t;
+        w.kv_lo = 0;
+        w.kv_hi = keys;
+        w.part = -1;
+        items.push_back(w);
+        continue;
+      }
+      const int ktiles = (keys + 63) / 64;
+      const int per = (ktiles + sp - 1) / sp * 64;
+      combines.push_back({t.row0, t.nrows, parts, 0});
+      for (int lo = 0; lo < keys; lo += per) {
+        TileDesc w = t;
+        w.kv_lo = lo;
+        w.kv_hi = std::min(keys, lo + per);
+        w.part = parts++;
+        items.push_back(w);
+        combines.back().nparts += 1;
+      }
+    }
+  }
 
   std::vector<std::int64_t> sw_in_req;
   for (int i = 0; i < p.n_ops; ++i)
@@ -653,7 +803,9 @@ void Impl::consume(const isim_batch_plan& p) {
   };
   const RowDesc* d_rows = reinterpret_cast<const RowDesc*>(put(rows.data(), rows.size() * sizeof(RowDesc)));
   const std::int32_t* d_drows = reinterpret_cast<const std::int32_t*>(put(drows.data(), drows.size() * 4));
-  const TileDesc* d_tiles = reinterpret_cast<const TileDesc*>(put(tiles.data(), tiles.size() * sizeof(TileDesc)));
+  const TileDesc* d_tiles = reinterpret_cast<const TileDesc*>(put(items.data(), items.size() * sizeof(TileDesc)));
+  const CombineDesc* d_combines =
+      reinterpret_cast<const CombineDesc*>(put(combines.data(), combines.size() * sizeof(CombineDesc)));
   const std::int32_t* d_samples = reinterpret_cast<const std::int32_t*>(put(samples.data(), samples.size() * 4));
   const std::int32_t* d_frees0 = reinterpret_cast<const std::int32_t*>(put(frees0.data(), frees0.size() * 4));
   const std::int32_t* d_allocs0 = reinterpret_cast<const std::int32_t*>(put(allocs0.data(), allocs0.size() * 4));
@@ -661,8 +813,8 @@ void Impl::consume(const isim_batch_plan& p) {
   IB2_CUDA(cudaEventRecord(plan_done_[k], main_));
   h2d_bytes_ += static_cast<std::int64_t>(off);
 
-  // ---- pre-phase: last iteration's swap-in scatter, block table, swap-in H2D ----
-  flush_swap_ins();
+  // ---- pre-phase: scatters this plan depends on, block table, swap-in H2D -----
+  flush_swap_ins_for(p);
   launch_block_update(table_, stack_, top_, err_, d_frees0, static_cast<int>(frees0.size()), d_allocs0,
                       static_cast<int>(allocs0.size()), main_);
   run_swaps(sw_in, sw_in_req, true);
@@ -673,13 +825,15 @@ void Impl::consume(const isim_batch_plan& p) {
     rows_dev_ = d_rows;
     drows_dev_ = d_drows;
     tiles_dev_ = d_tiles;
+    combines_dev_ = d_combines;
+    n_combines_ = static_cast<int>(combines.size());
     samples_dev_ = d_samples;
     std::int64_t k1_bytes = 0;
     for (int r : drows) k1_bytes += static_cast<std::int64_t>(rows[r].pos + 1) * 2 * spec_.d_model * 2;
     k1_bytes_iter_ = static_cast<double>(k1_bytes);
     max_pos1_ = 0;
     for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
-    forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(tiles.size()), static_cast<int>(samples.size()));
+    forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(items.size()), static_cast<int>(samples.size()));
     if (!samples.empty() && !record_) {
       IB2_CUDA(cudaEventSynchronize(tok_done_[k]));
       IB2_CUDA(cudaMemcpyAsync(tok_host_[k], out_tok_, samples.size() * 4, cudaMemcpyDeviceToHost, main_));
@@ -716,7 +870,7 @@ void Impl::consume(const isim_batch_plan& p) {
     }
     auto ex = extents_.find(rid);
     if (ex != extents_.end()) {
-      for (const Extent& x : ex->second) arena_.release(x.off, x.bytes);
+      for (const Extent& x : ex->second) release_extent_memory(x.off, x.bytes);
       extents_.erase(ex);
     }
   }
@@ -727,11 +881,18 @@ void Impl::consume(const isim_batch_plan& p) {
   decode_rows_total_ += static_cast<std::int64_t>(drows.size());
   chunk_rows_total_ += n_rows - static_cast<std::int64_t>(drows.size());
   samples_total_ += static_cast<std::int64_t>(samples.size());
-  for (const auto& s : sw_in) swap_in_tok_ += s.n;
-  for (const auto& s : sw_out) swap_out_tok_ += s.n;
+  std::int64_t it_in = 0, it_out = 0;
+  for (const auto& s : sw_in) it_in += s.n;
+  for (const auto& s : sw_out) it_out += s.n;
+  swap_in_tok_ += it_in;
+  swap_out_tok_ += it_out;
+  if (trace_iters_)
+    iter_info_.push_back({n_rows, static_cast<std::int64_t>(drows.size()), n_rows - static_cast<std::int64_t>(drows.size()),
+                          it_in, it_out});
   if (record_) {
     flush_swap_ins();
     IB2_CUDA(cudaStreamSynchronize(copy_));
+    IB2_CUDA(cudaStreamSynchronize(copy_in_));
     IB2_CUDA(cudaStreamSynchronize(main_));
     check_error();
     last_tok_.assign(p.n_spans, -1);
@@ -788,8 +949,9 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
       ev_pending_.push_back({e0, e1});
       ev_bytes_.push_back(k1_bytes_iter_ + static_cast<double>(n_drows) * 2.0 * D * 2);
     }
-    launch_chunk_attention(qkv_, tiles_dev_, n_tiles, g, l, attn_, main_);
-    if (n_tiles) ++kernel_launches_;
+    launch_chunk_attention(qkv_, tiles_dev_, n_tiles, combines_dev_, n_combines_, g, l, attn_, chunk_ws_o_,
+                           chunk_ws_ml_, main_);
+    if (n_tiles) kernel_launches_ += n_combines_ > 0 ? 2 : 1;
     if (m.parallel_residual()) {
       // GPT-J: x += attn W_o + mlp(ln1(x)); both read the same xn.
       gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
@@ -825,6 +987,7 @@ void Impl::sync() {
   flush_swap_ins();
   IB2_CUDA(cudaStreamSynchronize(main_));
   IB2_CUDA(cudaStreamSynchronize(copy_));
+  IB2_CUDA(cudaStreamSynchronize(copy_in_));
   check_error();
   for (std::size_t i = 0; i < ev_pending_.size(); ++i) {
     float ms = 0.f;
@@ -845,6 +1008,15 @@ void Impl::sync() {
   }
   swap_ev_pending_.clear();
   swap_ev_bytes_.clear();
+  if (trace_iters_ && iter_ev_.size() > 1) {
+    for (std::size_t i = 0; i + 1 < iter_ev_.size(); ++i) {
+      float ms = 0.f;
+      IB2_CUDA(cudaEventElapsedTime(&ms, iter_ev_[i], iter_ev_[i + 1]));
+      iter_ms_.push_back(ms);
+    }
+    for (std::size_t i = 0; i + 1 < iter_ev_.size(); ++i) cudaEventDestroy(iter_ev_[i]);
+    iter_ev_.erase(iter_ev_.begin(), iter_ev_.end() - 1);
+  }
 }
 
 cudaEvent_t Impl::new_timing_event() {
@@ -902,6 +1074,10 @@ std::string Impl::stats_json() const {
   j["swap_ms"] = swap_ms_;
   j["swap_bytes_timed"] = swap_bytes_timed_;
   j["kv_bytes_per_token"] = spec_.kv_bytes_per_token();
+  if (trace_iters_) {
+    j["iter_ms"] = iter_ms_;
+    j["iter_info"] = iter_info_;
+  }
   return j.dump();
 }
 
@@ -944,6 +1120,7 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
   const std::int64_t n = hi - lo;
   if (cap < n * L * 2 * D * 2) throw DeviceError("read_kv: buffer too small");
   IB2_CUDA(cudaStreamSynchronize(copy_));
+  IB2_CUDA(cudaStreamSynchronize(copy_in_));
   IB2_CUDA(cudaStreamSynchronize(main_));
   std::vector<std::int32_t> t(max_lb_);
   IB2_CUDA(cudaMemcpy(t.data(), table_ + static_cast<std::int64_t>(it->second) * max_lb_, max_lb_ * 4,

@@ -40,6 +40,8 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
     const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
     const std::int32_t* __restrict__ table, int max_lb, int H, int max_splits, float* __restrict__ part_o,
     float* __restrict__ part_ml) {
+  pdl_trigger();
+  pdl_wait();
   constexpr int LPT = HD / 8;   // lanes per token
   constexpr int TPW = 32 / LPT; // tokens per warp step
   const int split = blockIdx.x, h = blockIdx.y, dr = blockIdx.z;
@@ -159,6 +161,8 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
 __global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows, int H,
                                       int HD, int max_splits, const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, f16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
   const int dr = blockIdx.x, h = blockIdx.y;
   const int r = drow[dr];
   const int ns = (rows[r].pos + 1 + kSplit - 1) / kSplit;
@@ -227,7 +231,10 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
                                                          const f16* __restrict__ pool, std::int64_t layer_off,
                                                          std::int64_t block_stride,
                                                          const std::int32_t* __restrict__ table, int max_lb, int H,
-                                                         f16* __restrict__ out) {
+                                                         f16* __restrict__ out, float* __restrict__ ws_o,
+                                                         float* __restrict__ ws_ml) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   f16* sQ = reinterpret_cast<f16*>(smem_raw);
   f16* sK = sQ + kTileQ * HD;
@@ -238,6 +245,7 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const std::int32_t* tab = table + static_cast<std::int64_t>(td.slot) * max_lb;
   const int last_pos = td.pos0 + td.nrows - 1;
+  const int kv_hi = min(td.kv_hi, last_pos + 1);
   const f16* base = pool + layer_off;
 
   // Q tile (rows beyond nrows load zeros).
@@ -261,13 +269,13 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
   const int qp0 = td.pos0 + min(qrow0 + g, td.nrows - 1);
   const int qp1 = td.pos0 + min(qrow0 + g + 8, td.nrows - 1);
 
-  const int n_kt = last_pos / kTileK + 1;
-  for (int kt = 0; kt < n_kt; ++kt) {
+  const int kt_end = (kv_hi + kTileK - 1) / kTileK;
+  for (int kt = td.kv_lo / kTileK; kt < kt_end; ++kt) {
     __syncthreads();  // previous tile consumed
     for (int i = tid; i < kTileK * (HD / 8); i += 128) {
       const int row = i / (HD / 8), ch = i % (HD / 8);
       const int p = kt * kTileK + row;
-      const bool ok = p <= last_pos;
+      const bool ok = p < kv_hi;
       std::int64_t off = 0;
       if (ok) off = static_cast<std::int64_t>(tab[p / kBlockTokens]) * block_stride + (p % kBlockTokens) * HD + ch * 8;
       const f16* ksrc = base + off + (static_cast<std::int64_t>(h) * kBlockTokens) * HD;
@@ -305,10 +313,11 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
       const int kp = kt * kTileK + j * 8 + 2 * t4;
-      s[j][0] = kp <= qp0 ? s[j][0] * sc : -FLT_MAX;
-      s[j][1] = kp + 1 <= qp0 ? s[j][1] * sc : -FLT_MAX;
-      s[j][2] = kp <= qp1 ? s[j][2] * sc : -FLT_MAX;
-      s[j][3] = kp + 1 <= qp1 ? s[j][3] * sc : -FLT_MAX;
+      const bool in0 = kp >= td.kv_lo && kp < kv_hi, in1 = kp + 1 >= td.kv_lo && kp + 1 < kv_hi;
+      s[j][0] = in0 && kp <= qp0 ? s[j][0] * sc : -FLT_MAX;
+      s[j][1] = in1 && kp + 1 <= qp0 ? s[j][1] * sc : -FLT_MAX;
+      s[j][2] = in0 && kp <= qp1 ? s[j][2] * sc : -FLT_MAX;
+      s[j][3] = in1 && kp + 1 <= qp1 ? s[j][3] * sc : -FLT_MAX;
       mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
       mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
     }
@@ -317,9 +326,14 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
       mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o2));
       mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o2));
     }
-    const float corr0 = exp2f(m_r[0] - mx0), corr1 = exp2f(m_r[1] - mx1);
+    // Rows with no visible key yet (split-KV) keep m = -inf: exponentiate
+    // against 0 so masked scores give exactly 0.
+    const float e0 = mx0 == -FLT_MAX ? 0.f : mx0, e1 = mx1 == -FLT_MAX ? 0.f : mx1;
+    const float corr0 = exp2f(m_r[0] - e0), corr1 = exp2f(m_r[1] - e1);
     m_r[0] = mx0;
     m_r[1] = mx1;
+    mx0 = e0;
+    mx1 = e1;
     float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -359,29 +373,72 @@ __global__ void __launch_bounds__(128) chunk_attn_kernel(const f16* __restrict__
       }
     }
   }
-  // Row sums across the quad, normalize, store.
+  // Row sums across the quad; whole items normalize and store, split items
+  // leave an fp32 partial (unnormalized o, running max m, sum l).
 #pragma unroll
   for (int o2 = 1; o2 < 4; o2 <<= 1) {
     l_r[0] += __shfl_xor_sync(0xffffffffu, l_r[0], o2);
     l_r[1] += __shfl_xor_sync(0xffffffffu, l_r[1], o2);
   }
-  const float inv0 = 1.f / l_r[0], inv1 = 1.f / l_r[1];
   const int r0 = qrow0 + g, r1 = qrow0 + g + 8;
+  if (td.part < 0) {
+    const float inv0 = 1.f / l_r[0], inv1 = 1.f / l_r[1];
 #pragma unroll
-  for (int i = 0; i < DT; ++i) {
-    const int col = h * HD + i * 8 + 2 * t4;
-    if (r0 < td.nrows)
-      *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r0) * D + col) =
-          __floats2half2_rn(o[i][0] * inv0, o[i][1] * inv0);
-    if (r1 < td.nrows)
-      *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r1) * D + col) =
-          __floats2half2_rn(o[i][2] * inv1, o[i][3] * inv1);
+    for (int i = 0; i < DT; ++i) {
+      const int col = h * HD + i * 8 + 2 * t4;
+      if (r0 < td.nrows)
+        *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r0) * D + col) =
+            __floats2half2_rn(o[i][0] * inv0, o[i][1] * inv0);
+      if (r1 < td.nrows)
+        *reinterpret_cast<__half2*>(out + static_cast<std::int64_t>(td.row0 + r1) * D + col) =
+            __floats2half2_rn(o[i][2] * inv1, o[i][3] * inv1);
+    }
+  } else {
+    const std::int64_t slot = (static_cast<std::int64_t>(td.part) * H + h) * kTileQ;
+#pragma unroll
+    for (int i = 0; i < DT; ++i) {
+      const int col = i * 8 + 2 * t4;
+      *reinterpret_cast<float2*>(ws_o + (slot + r0) * HD + col) = make_float2(o[i][0], o[i][1]);
+      *reinterpret_cast<float2*>(ws_o + (slot + r1) * HD + col) = make_float2(o[i][2], o[i][3]);
+    }
+    if (t4 == 0) {
+      ws_ml[(slot + r0) * 2] = m_r[0];
+      ws_ml[(slot + r0) * 2 + 1] = l_r[0];
+      ws_ml[(slot + r1) * 2] = m_r[1];
+      ws_ml[(slot + r1) * 2 + 1] = l_r[1];
+    }
+  }
+}
+
+// Merge the split-KV partials of one q-tile and head.
+__global__ void chunk_combine_kernel(const CombineDesc* __restrict__ cds, int H, int HD,
+                                     const float* __restrict__ ws_o, const float* __restrict__ ws_ml,
+                                     f16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const CombineDesc c = cds[blockIdx.x];
+  const int h = blockIdx.y;
+  const int D = H * HD;
+  for (int e = threadIdx.x; e < c.nrows * HD; e += blockDim.x) {
+    const int r = e / HD, d = e % HD;
+    float M = -FLT_MAX;
+    for (int p = 0; p < c.nparts; ++p)
+      M = fmaxf(M, ws_ml[((static_cast<std::int64_t>(c.part0 + p) * H + h) * kTileQ + r) * 2]);
+    float L = 0.f, O = 0.f;
+    for (int p = 0; p < c.nparts; ++p) {
+      const std::int64_t slot = (static_cast<std::int64_t>(c.part0 + p) * H + h) * kTileQ + r;
+      const float m = ws_ml[slot * 2];
+      const float w = m == -FLT_MAX ? 0.f : exp2f(m - M);
+      L += ws_ml[slot * 2 + 1] * w;
+      O += ws_o[slot * HD + d] * w;
+    }
+    out[static_cast<std::int64_t>(c.row0 + r) * D + h * HD + d] = __float2half_rn(O / L);
   }
 }
 
 template <int HD>
 void launch_chunk_hd(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer, f16* out,
-                     cudaStream_t s) {
+                     float* ws_o, float* ws_ml, cudaStream_t s) {
   const int smem = (kTileQ + 2 * kTileK) * HD * 2;
   static bool configured = false;
   if (!configured) {
@@ -389,8 +446,8 @@ void launch_chunk_hd(const f16* qkv, const TileDesc* tiles, int n_tiles, const K
     configured = true;
   }
   dim3 grid(n_tiles, g.heads);
-  chunk_attn_kernel<HD><<<grid, 128, smem, s>>>(qkv, tiles, g.pool, layer * g.layer_stride(), g.block_stride(),
-                                                g.table, g.max_lblocks, g.heads, out);
+  launch_pdl(chunk_attn_kernel<HD>, grid, dim3(128), smem, s, qkv, tiles, g.pool, layer * g.layer_stride(),
+             g.block_stride(), g.table, g.max_lblocks, g.heads, out, ws_o, ws_ml);
   IB2_LAUNCH_CHECK();
 }
 
@@ -398,11 +455,11 @@ template <int HD>
 void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
                       int layer, int max_splits, float* part_o, float* part_ml, f16* out, cudaStream_t s) {
   dim3 grid(max_splits, g.heads, n);
-  decode_attn_kernel<HD><<<grid, kDecWarps * 32, 0, s>>>(qkv, drow, rows, g.pool, layer * g.layer_stride(),
-                                                         g.block_stride(), g.table, g.max_lblocks, g.heads,
-                                                         max_splits, part_o, part_ml);
+  launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
+             layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml);
   IB2_LAUNCH_CHECK();
-  decode_combine_kernel<<<dim3(n, g.heads), HD, 0, s>>>(drow, rows, g.heads, HD, max_splits, part_o, part_ml, out);
+  launch_pdl(decode_combine_kernel, dim3(n, g.heads), dim3(HD), 0, s, drow, rows, g.heads, HD, max_splits, part_o,
+             part_ml, out);
   IB2_LAUNCH_CHECK();
 }
 
@@ -421,15 +478,19 @@ void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const Row
   }
 }
 
-void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
-                            f16* out, cudaStream_t s) {
+void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const CombineDesc* combines,
+                            int n_combines, const KvGeom& g, int layer, f16* out, float* ws_o, float* ws_ml,
+                            cudaStream_t s) {
   if (n_tiles <= 0) return;
   switch (g.head_dim) {
-    case 64: launch_chunk_hd<64>(qkv, tiles, n_tiles, g, layer, out, s); break;
-    case 128: launch_chunk_hd<128>(qkv, tiles, n_tiles, g, layer, out, s); break;
-    case 256: launch_chunk_hd<256>(qkv, tiles, n_tiles, g, layer, out, s); break;
+    case 64: launch_chunk_hd<64>(qkv, tiles, n_tiles, g, layer, out, ws_o, ws_ml, s); break;
+    case 128: launch_chunk_hd<128>(qkv, tiles, n_tiles, g, layer, out, ws_o, ws_ml, s); break;
+    case 256: launch_chunk_hd<256>(qkv, tiles, n_tiles, g, layer, out, ws_o, ws_ml, s); break;
     default: throw DeviceError("unsupported head_dim");
   }
+  if (n_combines > 0)
+    launch_pdl(chunk_combine_kernel, dim3(n_combines, g.heads), dim3(256), 0, s, combines, g.heads, g.head_dim, ws_o,
+               ws_ml, out);
 }
 
 int decode_split_positions() { return kSplit; }

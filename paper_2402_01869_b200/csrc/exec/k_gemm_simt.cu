@@ -12,6 +12,8 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 32;
 
 __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs a) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sA[BK][BM + 4];
   __shared__ float sW[BK][BN + 4];
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(GemmArgs a) {
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
   if (a.M <= 0) return;
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
-  simt_gemm_kernel<<<grid, 256, 0, s>>>(a);
+  launch_pdl(simt_gemm_kernel, grid, dim3(256), 0, s, a);
   IB2_LAUNCH_CHECK();
 }
 

@@ -105,7 +105,9 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  // M-fastest rasterization: the M tiles that share a weight tile run in the
+  // same wave, so the weight tile is fetched from HBM once and re-read from L2.
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int nk = (args.K + BK - 1) / BK;
 
   if (warp == 0 && lane == 0) {
@@ -127,6 +129,8 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the prologue above overlapped the predecessor kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -320,6 +324,8 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the prologue above overlapped the predecessor kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -396,35 +402,40 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
     }
   }
   if (SPLIT > 1) {
-    // Partials are in every CTA's shared memory: rank 0 sums them in rank order.
+    // Partials sit in every CTA's shared memory.  Rank r reduces token
+    // columns [r*M/SPLIT, (r+1)*M/SPLIT) over DSMEM, always summing ranks in
+    // order 0..SPLIT-1 (deterministic), then runs the fused epilogue.
     cluster_sync_all();
-    if (rank == 0 && warp >= 4) {
+    if (warp >= 4) {
       const int row = (warp - 4) * 32 + lane, n = t0 * BM + row;
       const std::uint32_t local = su32(smem);
       std::uint32_t peer[SPLIT];
 #pragma unroll
       for (int r = 0; r < SPLIT; ++r)
         asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer[r]) : "r"(local), "r"(r));
-      for (int m0 = 0; m0 < args.M; m0 += 8) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+      const int m_lo = rank * args.M / SPLIT, m_hi = (rank + 1) * args.M / SPLIT;
+      for (int m0 = m_lo; m0 < m_hi; m0 += 16) {
+        float x[SPLIT][16];
 #pragma unroll
         for (int r = 0; r < SPLIT; ++r)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float x = 0.f;
-            if (m0 + j < args.M)
+          for (int j = 0; j < 16; ++j) {
+            x[r][j] = 0.f;
+            if (m0 + j < m_hi)
               asm volatile("ld.shared::cluster.f32 %0, [%1];\n"
-                           : "=f"(x)
+                           : "=f"(x[r][j])
                            : "r"(peer[r] + static_cast<std::uint32_t>(((m0 + j) * BM + row) * 4)));
-            v[j] += x;
           }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) epi_row(args, n, m0 + j, v[j], lane);
+        for (int j = 0; j < 16; ++j) {
+          float v = 0.f;
+#pragma unroll
+          for (int r = 0; r < SPLIT; ++r) v += x[r][j];
+          if (m0 + j < m_hi) epi_row(args, n, m0 + j, v, lane);
+        }
       }
     }
-    cluster_sync_all();  // peers' shared memory stays alive until rank 0 is done
+    cluster_sync_all();  // peers' shared memory stays alive until every rank is done
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -505,9 +516,8 @@ void launch_tc(const GemmArgs& a, cudaStream_t s) {
   const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, BM);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN == 256 ? 128 : BN);
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM);
-  tc_gemm_kernel<BN, STAGES><<<grid, 256, L::TOTAL, s>>>(ma, mw, a);
-  IB2_LAUNCH_CHECK();
+  dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN);
+  launch_pdl(tc_gemm_kernel<BN, STAGES>, grid, dim3(256), L::TOTAL, s, ma, mw, a);
 }
 
 
@@ -530,13 +540,15 @@ void launch_skinny(const GemmArgs& a, int ctas, cudaStream_t s) {
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = SPLIT;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_skinny_kernel<NT, STAGES, SPLIT>, mw, ma, a));
 }
 

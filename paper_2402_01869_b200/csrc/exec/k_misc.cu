@@ -77,6 +77,8 @@ __global__ void fill_kernel(std::int32_t* p, std::int64_t n, std::int32_t v) {
 __global__ void embed_kernel(const RowDesc* __restrict__ rows, std::int32_t* __restrict__ hist, int hist_stride,
                              const f16* __restrict__ tok_emb, const f16* __restrict__ pos_emb, int D,
                              std::uint64_t token_seed, int vocab, float* __restrict__ x) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const RowDesc d = rows[r];
   std::int32_t* h = hist + static_cast<std::int64_t>(d.slot) * hist_stride + d.pos;
@@ -108,6 +110,8 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, i
                                                   const std::int32_t* __restrict__ row_index, int D,
                                                   const f16* __restrict__ gamma, const f16* __restrict__ beta,
                                                   int rms, float eps, f16* __restrict__ y, int ldy) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float red[NT / 32];
   const int r = blockIdx.x;
   const int src = row_index ? row_index[r] : r;
@@ -149,6 +153,8 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, i
 __global__ void rope_kv_kernel(f16* __restrict__ qkv, const RowDesc* __restrict__ rows, f16* __restrict__ pool,
                                std::int64_t layer_off, std::int64_t block_stride, const std::int32_t* __restrict__ table,
                                int max_lb, int H, int hd, int rot, int interleaved, const float* __restrict__ cs) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const RowDesc d = rows[r];
   const int D = H * hd;
@@ -191,6 +197,8 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
                                                    const std::int32_t* __restrict__ sample_rows,
                                                    const RowDesc* __restrict__ rows, std::int32_t* __restrict__ hist,
                                                    int hist_stride, std::int32_t* __restrict__ out_tok) {
+  pdl_trigger();
+  pdl_wait();
   const int s = blockIdx.x;
   const float* l = logits + static_cast<std::int64_t>(s) * V;
   float best = -FLT_MAX;
@@ -232,6 +240,8 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
 
 __global__ void gather_rows_kernel(const f16* __restrict__ src, int ld, const std::int32_t* __restrict__ rows, int D,
                                    f16* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x;
   const uint4* s = reinterpret_cast<const uint4*>(src + static_cast<std::int64_t>(rows[r]) * ld);
   uint4* d = reinterpret_cast<uint4*>(dst + static_cast<std::int64_t>(r) * D);
@@ -246,6 +256,8 @@ __global__ void __launch_bounds__(1024) block_update_kernel(std::int32_t* __rest
                                                             std::int32_t* __restrict__ err,
                                                             const std::int32_t* __restrict__ frees, int nf,
                                                             const std::int32_t* __restrict__ allocs, int na) {
+  pdl_trigger();
+  pdl_wait();
   const int t0 = *top;
   for (int k = threadIdx.x; k < nf; k += blockDim.x) {
     const int e = frees[k];
@@ -273,6 +285,8 @@ __global__ void swap_copy_kernel(const SwapDesc* __restrict__ ops, const std::in
                                  f16* __restrict__ pool, std::int64_t layer_stride, std::int64_t block_stride,
                                  const std::int32_t* __restrict__ table, int max_lb, int H, int hd,
                                  f16* __restrict__ stage, int to_stage) {
+  pdl_trigger();
+  pdl_wait();
   const int t = blockIdx.x, layer = blockIdx.y;
   int lo = 0, hi = n_ops;  // find op with prefix[op] <= t < prefix[op+1]
   while (hi - lo > 1) {
@@ -330,7 +344,7 @@ void launch_fill_i32(std::int32_t* p, std::int64_t n, std::int32_t v, cudaStream
 void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_stride, const f16* tok_emb,
                   const f16* pos_emb, int D, std::uint64_t token_seed, int vocab, float* x, cudaStream_t s) {
   if (n <= 0) return;
-  embed_kernel<<<n, 256, 0, s>>>(rows, hist, hist_stride, tok_emb, pos_emb, D, token_seed, vocab, x);
+  launch_pdl(embed_kernel, dim3(n), dim3(256), 0, s, rows, hist, hist_stride, tok_emb, pos_emb, D, token_seed, vocab, x);
   IB2_LAUNCH_CHECK();
 }
 
@@ -338,11 +352,11 @@ void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, 
                  const f16* beta, bool rms, float eps, f16* y, int ldy, cudaStream_t s) {
   if (n <= 0) return;
   if (D <= 1024) {
-    norm_kernel<256, 4><<<n, 256, 0, s>>>(x, ldx, row_index, D, gamma, beta, rms, eps, y, ldy);
+    launch_pdl(norm_kernel<256, 4>, dim3(n), dim3(256), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
   } else if (D <= 4096) {
-    norm_kernel<512, 8><<<n, 512, 0, s>>>(x, ldx, row_index, D, gamma, beta, rms, eps, y, ldy);
+    launch_pdl(norm_kernel<512, 8>, dim3(n), dim3(512), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
   } else {
-    norm_kernel<512, 16><<<n, 512, 0, s>>>(x, ldx, row_index, D, gamma, beta, rms, eps, y, ldy);
+    launch_pdl(norm_kernel<512, 16>, dim3(n), dim3(512), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
   }
   IB2_LAUNCH_CHECK();
 }
@@ -350,29 +364,29 @@ void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, 
 void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
                           bool interleaved, const float* rope_cs, cudaStream_t s) {
   if (n <= 0) return;
-  rope_kv_kernel<<<n, 256, 0, s>>>(qkv, rows, g.pool, layer * g.layer_stride(), g.block_stride(), g.table,
-                                   g.max_lblocks, g.heads, g.head_dim, rotary_dim, interleaved ? 1 : 0, rope_cs);
+  launch_pdl(rope_kv_kernel, dim3(n), dim3(256), 0, s, qkv, rows, g.pool, layer * g.layer_stride(), g.block_stride(),
+             g.table, g.max_lblocks, g.heads, g.head_dim, rotary_dim, interleaved ? 1 : 0, rope_cs);
   IB2_LAUNCH_CHECK();
 }
 
 void launch_argmax(const float* logits, int n, int V, const std::int32_t* sample_rows, const RowDesc* rows,
                    std::int32_t* hist, int hist_stride, std::int32_t* out_tok, cudaStream_t s) {
   if (n <= 0) return;
-  argmax_kernel<512><<<n, 512, 0, s>>>(logits, V, sample_rows, rows, hist, hist_stride, out_tok);
+  launch_pdl(argmax_kernel<512>, dim3(n), dim3(512), 0, s, logits, V, sample_rows, rows, hist, hist_stride, out_tok);
   IB2_LAUNCH_CHECK();
 }
 
 void launch_gather_rows(const f16* src, int ld, const std::int32_t* rows, int n, int D, f16* dst,
                         cudaStream_t s) {
   if (n <= 0) return;
-  gather_rows_kernel<<<n, 256, 0, s>>>(src, ld, rows, D, dst);
+  launch_pdl(gather_rows_kernel, dim3(n), dim3(256), 0, s, src, ld, rows, D, dst);
   IB2_LAUNCH_CHECK();
 }
 
 void launch_block_update(std::int32_t* table, std::int32_t* stack, std::int32_t* top, std::int32_t* err,
                          const std::int32_t* frees, int nf, const std::int32_t* allocs, int na, cudaStream_t s) {
   if (nf == 0 && na == 0) return;
-  block_update_kernel<<<1, 1024, 0, s>>>(table, stack, top, err, frees, nf, allocs, na);
+  launch_pdl(block_update_kernel, dim3(1), dim3(1024), 0, s, table, stack, top, err, frees, nf, allocs, na);
   IB2_LAUNCH_CHECK();
 }
 
@@ -380,8 +394,8 @@ void launch_swap_copy(const SwapDesc* ops, const std::int32_t* tok_prefix, int n
                       const KvGeom& g, f16* stage, bool to_stage, cudaStream_t s) {
   if (total_tokens <= 0) return;
   dim3 grid(total_tokens, g.layers);
-  swap_copy_kernel<<<grid, 256, 0, s>>>(ops, tok_prefix, n_ops, g.pool, g.layer_stride(), g.block_stride(),
-                                        g.table, g.max_lblocks, g.heads, g.head_dim, stage, to_stage ? 1 : 0);
+  launch_pdl(swap_copy_kernel, grid, dim3(256), 0, s, ops, tok_prefix, n_ops, g.pool, g.layer_stride(), g.block_stride(),
+             g.table, g.max_lblocks, g.heads, g.head_dim, stage, to_stage ? 1 : 0);
   IB2_LAUNCH_CHECK();
 }
 

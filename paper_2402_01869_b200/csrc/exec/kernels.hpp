@@ -42,9 +42,11 @@ void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const Row
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
                              f16* out, cudaStream_t s);
 
-// K2: tiled causal attention over the paged prefix for chunk rows.
-void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const KvGeom& g, int layer,
-                            f16* out, cudaStream_t s);
+// K2: tiled causal attention over the paged prefix for chunk rows, split-KV
+// items + combine pass for tiles whose keys were split.
+void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const CombineDesc* combines,
+                            int n_combines, const KvGeom& g, int layer, f16* out, float* ws_o, float* ws_ml,
+                            cudaStream_t s);
 
 // K3: projection GEMM with fused epilogue.
 void launch_gemm(const GemmArgs& a, cudaStream_t s);
