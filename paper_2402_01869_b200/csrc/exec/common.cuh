@@ -86,7 +86,7 @@ struct RowDesc {
 // (o, m, l) into slot `part` for the combine pass.
 struct TileDesc {
   std::int32_t row0;   // first batch row
-  std::int32_t nrows;  // <= 64
+  std::int32_t nrows;  // <= kChunkTileRows
   std::int32_t slot;
   std::int32_t pos0;   // position of row0
   std::int32_t kv_lo, kv_hi;
@@ -98,7 +98,8 @@ struct TileDesc {
 struct CombineDesc {
   std::int32_t row0, nrows, part0, nparts;
 };
-constexpr int kMaxChunkParts = 640;  // (part, head) slots of the split-KV workspace
+constexpr int kChunkTileRows = 128;  // query rows per K2 item (UMMA M)
+constexpr int kMaxChunkParts = 1024;  // (part, head) slots of the split-KV workspace
 
 // Swap copy descriptor: positions [pos0, pos0+n) of a slot <-> staging rows.
 struct SwapDesc {

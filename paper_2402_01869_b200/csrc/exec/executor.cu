@@ -352,8 +352,8 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   part_o_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * spec_.head_dim());
   part_ml_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * 2);
   set_gemm_activation_rows(max_rows_);
-  chunk_ws_o_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * 64 * spec_.head_dim());
-  chunk_ws_ml_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * 64 * 2);
+  chunk_ws_o_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * spec_.head_dim());
+  chunk_ws_ml_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * 2);
 
   // plan ring
   plan_bytes_ = static_cast<std::size_t>(max_rows_) * (sizeof(RowDesc) + 4 * 4) +
@@ -741,27 +741,30 @@ void Impl::consume(const isim_batch_plan& p) {
     if (sp.count == 1 || force_row_attention_) {
       for (int k = 0; k < sp.count; ++k) drows.push_back(r0 + k);
     } else {
-      for (int k = 0; k < sp.count; k += 64)
-        tiles.push_back({r0 + k, std::min(64, sp.count - k), slot, sp.pos + k, 0, 0, -1, 0});
+      for (int k = 0; k < sp.count; k += kChunkTileRows)
+        tiles.push_back({r0 + k, std::min(kChunkTileRows, sp.count - k), slot, sp.pos + k, 0, 0, -1, 0});
     }
     if (sp.sample) samples.push_back(r0 + sp.count - 1);
   }
   const int n_rows = static_cast<int>(rows.size());
   if (n_rows > max_rows_) throw DeviceError("executor: batch exceeds max_rows");
-  // Split-KV for chunk tiles: aim for ~2 waves of (item, head) CTAs; a tile's
-  // keys are split into 64-aligned ranges of >= 256 keys.
+  // Split-KV for chunk tiles (one CTA per SM: K2 holds 512 TMEM columns):
+  // key ranges of at most `per` keys, `per` ~ the whole (tile, head) key work
+  // spread over the SMs, at least 512 keys, aligned to K2's key tile.
   std::vector<TileDesc> items;
   std::vector<CombineDesc> combines;
   {
     const int H = spec_.heads;
-    const int base_ctas = static_cast<int>(tiles.size()) * H;
-    const int want = base_ctas > 0 ? std::max(1, (2 * 148 + base_ctas - 1) / base_ctas) : 1;
+    const int bn = chunk_attention_key_tile(spec_.head_dim());
+    std::int64_t work = 0;
+    for (const TileDesc& t : tiles) work += static_cast<std::int64_t>(t.pos0 + t.nrows) * H;
+    std::int64_t per = std::max<std::int64_t>(512, (work + 147) / 148);
+    per = (per + bn - 1) / bn * bn;
     int parts = 0;
     for (const TileDesc& t : tiles) {
       const int keys = t.pos0 + t.nrows;
-      int sp = std::min(want, std::max(1, keys / 256));
-      if ((parts + sp) * H > kMaxChunkParts) sp = 1;
-      if (sp == 1) {
+      const int sp = static_cast<int>((keys + per - 1) / per);
+      if (sp == 1 || (parts + sp) * H > kMaxChunkParts) {
         TileDesc w = t;
         w.kv_lo = 0;
         w.kv_hi = keys;
@@ -769,13 +772,14 @@ void Impl::consume(const isim_batch_plan& p) {
         items.push_back(w);
         continue;
       }
-      const int ktiles = (keys + 63) / 64;
-      const int per = (ktiles + sp - 1) / sp * 64;
+      // Even split in whole key tiles.
+      const int ktiles = (keys + bn - 1) / bn;
+      const int step = (ktiles + sp - 1) / sp * bn;
       combines.push_back({t.row0, t.nrows, parts, 0});
-      for (int lo = 0; lo < keys; lo += per) {
+      for (int lo = 0; lo < keys; lo += step) {
         TileDesc w = t;
         w.kv_lo = lo;
-        w.kv_hi = std::min(keys, lo + per);
+        w.kv_hi = std::min(keys, lo + step);
         w.part = parts++;
         items.push_back(w);
         combines.back().nparts += 1;
@@ -949,8 +953,8 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
       ev_pending_.push_back({e0, e1});
       ev_bytes_.push_back(k1_bytes_iter_ + static_cast<double>(n_drows) * 2.0 * D * 2);
     }
-    launch_chunk_attention(qkv_, tiles_dev_, n_tiles, combines_dev_, n_combines_, g, l, attn_, chunk_ws_o_,
-                           chunk_ws_ml_, main_);
+    launch_chunk_attention(qkv_, max_rows_, tiles_dev_, n_tiles, combines_dev_, n_combines_, g, l, attn_,
+                           chunk_ws_o_, chunk_ws_ml_, main_);
     if (n_tiles) kernel_launches_ += n_combines_ > 0 ? 2 : 1;
     if (m.parallel_residual()) {
       // GPT-J: x += attn W_o + mlp(ln1(x)); both read the same xn.

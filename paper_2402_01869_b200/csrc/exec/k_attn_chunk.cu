@@ -1,0 +1,431 @@
+// K2: chunk attention (prefill / recompute / API-returned tokens) over the
+// paged prefix on 5th-generation tensor cores.
+//
+// One CTA = one work item: a tile of up to 128 consecutive query rows of one
+// request, one head, restricted to keys [kv_lo, kv_hi) (split-KV).  Flash
+// attention with both contractions on tcgen05 and the accumulators in TMEM:
+//
+//   warp 0      TMA producer: the Q tile once ([128][hd] from the qkv
+//               activations), then per key tile the K and V rows of BN/16 paged
+//               blocks ([16][hd] each, contiguous in the pool) into a 2-stage
+//               ring, 128-byte swizzle;
+//   warp 1      MMA issuer: S_t = Q K_t^T (M=128, N=BN, K=hd; both operands
+//               K-major) into one of two TMEM S buffers, then O += P_{t-1} V_{t-1}
+//               (M=128, N=hd, K=BN; P K-major from shared memory, V MN-major
+//               straight from the TMA tile) -- S_t overlaps softmax(t-1);
+//   warp 2      TMEM allocator (512 columns: O = hd, S = 2 x BN);
+//   warps 4-7   softmax: thread = query row = TMEM lane.  Row max / exp2 / sum
+//               are thread-local (no shuffles); P is written f16 into swizzled
+//               shared memory; O is rescaled in TMEM only when the running max
+//               grew by more than 2^8 (the exact max used is tracked, so the
+//               final normalisation is exact); epilogue O / l -> f16 output, or
+//               an fp32 partial (O, m, l) for the combine kernel.
+//
+// Keys are visited in ascending block order, like K1.  Tensor-core
+// bound: 4 * rows * keys * hd FLOP per (item, head).
+#include <cfloat>
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels.hpp"
+#include "tc_ptx.cuh"
+
+namespace ib2 {
+
+namespace {
+
+using namespace tc;
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O when the max grew by > 2^8
+
+template <int HD>
+struct AttnCfg {
+  static constexpr int BQ = 128;
+  static constexpr int BN = HD == 256 ? 64 : 128;  // keys per tile
+  static constexpr int NCH = HD / 64;              // 64-wide head-dim chunks (one 128 B swizzle row)
+  static constexpr int STAGES = 2;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int KV_BYTES = BN * HD * 2;  // K or V tile
+  static constexpr int STAGE_BYTES = 2 * KV_BYTES;
+  static constexpr int P_BYTES = BQ * BN * 2;
+  static constexpr int KV_OFF = Q_BYTES;
+  static constexpr int P_OFF = KV_OFF + STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int S_COL = HD;  // S buffers after O
+  static_assert(HD + 2 * BN <= TMEM_COLS, "TMEM budget");
+  static_assert(TOTAL <= 232448, "shared memory budget");
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap map_q,
+                                                               const __grid_constant__ CUtensorMap map_kv,
+                                                               const TileDesc* __restrict__ items,
+                                                               const std::int32_t* __restrict__ table, int max_lb,
+                                                               std::int64_t layer_row0, int H,
+                                                               f16* __restrict__ out, float* __restrict__ ws_o,
+                                                               float* __restrict__ ws_ml) {
+  using C = AttnCfg<HD>;
+  constexpr int BQ = C::BQ, BN = C::BN, NCH = C::NCH, STAGES = C::STAGES;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem =
+      reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + C::BAR_OFF);
+  std::uint64_t* qfull = bars;                // 1
+  std::uint64_t* kvfull = bars + 1;           // STAGES
+  std::uint64_t* kvempty = kvfull + STAGES;   // STAGES
+  std::uint64_t* sfull = kvempty + STAGES;    // 2
+  std::uint64_t* sfree = sfull + 2;           // 2
+  std::uint64_t* pfull = sfree + 2;           // 1
+  std::uint64_t* pvdone = pfull + 1;          // 1
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(pvdone + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_q);
+    prefetch_map(&map_kv);
+    mbar_init(qfull, 1);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&kvfull[i], 1);
+      mbar_init(&kvempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1);
+      mbar_init(&sfree[i], 4);  // one arrival per softmax warp
+    }
+    mbar_init(pfull, 4);
+    mbar_init(pvdone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const std::uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // qkv, pool and block tables come from earlier kernels of this iteration
+
+  const TileDesc td = items[blockIdx.x];
+  const int last_pos = td.pos0 + td.nrows - 1;
+  const int kv_hi = min(td.kv_hi, last_pos + 1);
+  const int kt0 = td.kv_lo / BN;
+  const int nt = (kv_hi + BN - 1) / BN - kt0;
+  unsigned char* sQ = smem;
+  unsigned char* sKV = smem + C::KV_OFF;
+  unsigned char* sP = smem + C::P_OFF;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(qfull, C::Q_BYTES);
+#pragma unroll
+      for (int j = 0; j < NCH; ++j) tma_load_2d(sQ + j * BQ * 128, &map_q, qfull, h * HD + 64 * j, td.row0);
+      const std::int32_t* tab = table + static_cast<std::int64_t>(td.slot) * max_lb;
+      const int lb_last = (kv_hi - 1) / kBlockTokens;
+      for (int t = 0; t < nt; ++t) {
+        const int st = t % STAGES;
+        if (t >= STAGES) mbar_wait(&kvempty[st], ((t / STAGES) - 1) & 1);
+        mbar_expect_tx(&kvfull[st], C::STAGE_BYTES);
+        unsigned char* sK = sKV + st * C::STAGE_BYTES;
+        unsigned char* sV = sK + C::KV_BYTES;
+#pragma unroll 1
+        for (int b = 0; b < BN / kBlockTokens; ++b) {
+          // Blocks past the key range re-load the last valid block (finite
+          // values; their scores are masked to -inf, so P = 0 there).
+          const int lb = min((kt0 + t) * (BN / kBlockTokens) + b, lb_last);
+          const std::int64_t pb = tab[lb];
+          const int krow = static_cast<int>(layer_row0 + (pb * 2) * H * kBlockTokens + h * kBlockTokens);
+          const int vrow = krow + H * kBlockTokens;
+#pragma unroll
+          for (int j = 0; j < NCH; ++j) {
+            tma_load_2d(sK + j * BN * 128 + b * kBlockTokens * 128, &map_kv, &kvfull[st], 64 * j, krow);
+            tma_load_2d(sV + j * BN * 128 + b * kBlockTokens * 128, &map_kv, &kvfull[st], 64 * j, vrow);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr std::uint32_t idesc_s = idesc_f16(BQ, BN, false, false);
+      constexpr std::uint32_t idesc_pv = idesc_f16(BQ, HD, false, true);
+      const std::uint32_t q_base = su32(sQ), kv_base = su32(sKV), p_base = su32(sP);
+      auto issue_pv = [&](int u) {
+        mbar_wait(pfull, u & 1);
+        fence_after();
+        const std::uint32_t v_base = kv_base + (u % STAGES) * C::STAGE_BYTES + C::KV_BYTES;
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          const std::uint64_t da = desc_sw128(p_base + (k / 4) * BQ * 128 + (k % 4) * 32, 16, 1024);
+          const std::uint64_t db = desc_sw128(v_base + k * 16 * 128, BN * 128, 1024);
+          mma_f16(tmem, da, db, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(pvdone);
+        mma_commit(&kvempty[u % STAGES]);
+      };
+      mbar_wait(qfull, 0);
+      for (int t = 0; t < nt; ++t) {
+        const int st = t % STAGES, b = t & 1;
+        mbar_wait(&kvfull[st], (t / STAGES) & 1);
+        if (t >= 2) mbar_wait(&sfree[b], ((t / 2) - 1) & 1);
+        fence_after();
+        const std::uint32_t k_base = kv_base + st * C::STAGE_BYTES;
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const std::uint64_t da = desc_sw128(q_base + (k / 4) * BQ * 128 + (k % 4) * 32, 16, 1024);
+          const std::uint64_t db = desc_sw128(k_base + (k / 4) * BN * 128 + (k % 4) * 32, 16, 1024);
+          mma_f16(tmem + C::S_COL + b * BN, da, db, idesc_s, k > 0 ? 1u : 0u);
+        }
+        mma_commit(&sfull[b]);
+        if (t >= 1) issue_pv(t - 1);
+      }
+      issue_pv(nt - 1);
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const int r = q * 32 + lane;  // query row of this thread = TMEM lane
+    const std::uint32_t lane_off = static_cast<std::uint32_t>(q * 32) << 16;
+    const int qp = td.pos0 + min(r, td.nrows - 1);
+    const float sc = rsqrtf(static_cast<float>(HD)) * kLog2e;
+    float m_used = -FLT_MAX;  // max the exponentials are taken against (log2 units)
+    float l = 0.f;
+    for (int t = 0; t < nt; ++t) {
+      const int b = t & 1;
+      mbar_wait(&sfull[b], (t / 2) & 1);
+      fence_after();
+      float s[BN];
+      {
+        std::uint32_t raw[BN];
+#pragma unroll
+        for (int c = 0; c < BN; c += 16) tmem_ld16_nowait(tmem + lane_off + C::S_COL + b * BN + c, raw + c);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < BN; ++i) s[i] = __uint_as_float(raw[i]);
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sfree[b]);
+
+      const int k0 = (kt0 + t) * BN;
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int i = 0; i < BN; ++i) {
+        const int kp = k0 + i;
+        const bool ok = kp >= td.kv_lo && kp < kv_hi && kp <= qp;
+        s[i] = ok ? s[i] * sc : -FLT_MAX;
+        mx = fmaxf(mx, s[i]);
+      }
+      float factor = 1.f;
+      bool rescale = false;
+      if (mx > -FLT_MAX) {
+        if (m_used == -FLT_MAX) {
+          m_used = mx;  // O holds only zero contributions so far
+        } else if (mx > m_used + kRescaleThreshold) {
+          factor = exp2f(m_used - mx);
+          m_used = mx;
+          rescale = true;
+        }
+      }
+      l *= factor;
+      // P = exp2(s - m_used) rounded to f16; the row sum uses the same rounded
+      // values so numerator and denominator agree.
+      std::uint32_t pk[BN / 2];
+#pragma unroll
+      for (int i = 0; i < BN; i += 2) {
+        const float e0 = s[i] == -FLT_MAX ? 0.f : exp2f(s[i] - m_used);
+        const float e1 = s[i + 1] == -FLT_MAX ? 0.f : exp2f(s[i + 1] - m_used);
+        const __half2 hv = __floats2half2_rn(e0, e1);
+        const float2 back = __half22float2(hv);
+        l += back.x + back.y;
+        pk[i / 2] = *reinterpret_cast<const std::uint32_t*>(&hv);
+      }
+      // P buffer and O are free once PV(t-1) retired.
+      if (t >= 1) {
+        mbar_wait(pvdone, (t - 1) & 1);
+        fence_after();
+        if (__any_sync(0xffffffffu, rescale)) {
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 16) {
+            std::uint32_t o[16];
+            tmem_ld16_nowait(tmem + lane_off + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            tmem_st16(tmem + lane_off + c, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P row -> shared memory, K-major 128 B swizzle: 16 B unit u of row r
+      // lands at unit u ^ (r & 7) of the row's 128 B line.
+#pragma unroll
+      for (int u = 0; u < BN / 8; ++u) {
+        const int ch = u / 8, uu = u % 8;
+        uint4 v;
+        v.x = pk[u * 4 + 0];
+        v.y = pk[u * 4 + 1];
+        v.z = pk[u * 4 + 2];
+        v.w = pk[u * 4 + 3];
+        *reinterpret_cast<uint4*>(sP + ch * BQ * 128 + r * 128 + ((uu ^ (r & 7)) * 16)) = v;
+      }
+      fence_proxy_async();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pfull);
+    }
+    // Epilogue.
+    mbar_wait(pvdone, (nt - 1) & 1);
+    fence_after();
+    if (td.part < 0) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      f16* dst = out + static_cast<std::int64_t>(td.row0 + r) * H * HD + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 16) {
+        std::uint32_t o[16];
+        tmem_ld16_nowait(tmem + lane_off + c, o);
+        tmem_wait_ld();
+        if (r < td.nrows) {
+          uint4 v[2];
+          std::uint32_t* w = reinterpret_cast<std::uint32_t*>(v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const __half2 hv = __floats2half2_rn(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
+            w[i] = *reinterpret_cast<const std::uint32_t*>(&hv);
+          }
+          *reinterpret_cast<uint4*>(dst + c) = v[0];
+          *reinterpret_cast<uint4*>(dst + c + 8) = v[1];
+        }
+      }
+    } else {
+      const std::int64_t slot = (static_cast<std::int64_t>(td.part) * H + h) * BQ + r;
+      float* dst = ws_o + slot * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 16) {
+        std::uint32_t o[16];
+        tmem_ld16_nowait(tmem + lane_off + c, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(dst + c + i) = make_float4(__uint_as_float(o[i]), __uint_as_float(o[i + 1]),
+                                                                __uint_as_float(o[i + 2]), __uint_as_float(o[i + 3]));
+      }
+      ws_ml[slot * 2] = m_used;
+      ws_ml[slot * 2 + 1] = l;
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    fence_after();
+    tmem_dealloc(tmem, C::TMEM_COLS);
+  }
+}
+
+// Merge the split-KV partials of one q-tile: one warp per (row, head); the
+// lanes own hd/32 consecutive columns.
+__global__ void __launch_bounds__(256) chunk_combine_kernel(const CombineDesc* __restrict__ cds, int H, int HD,
+                                                            const float* __restrict__ ws_o,
+                                                            const float* __restrict__ ws_ml, f16* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const CombineDesc c = cds[blockIdx.x];
+  const int h = blockIdx.y;
+  const int r = blockIdx.z * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= c.nrows) return;
+  float M = -FLT_MAX;
+  for (int p = 0; p < c.nparts; ++p)
+    M = fmaxf(M, ws_ml[((static_cast<std::int64_t>(c.part0 + p) * H + h) * kChunkTileRows + r) * 2]);
+  const int per = HD / 32;  // 2, 4 or 8 columns per lane
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  float L = 0.f;
+  for (int p = 0; p < c.nparts; ++p) {
+    const std::int64_t slot = (static_cast<std::int64_t>(c.part0 + p) * H + h) * kChunkTileRows + r;
+    const float m = ws_ml[slot * 2];
+    const float w = m == -FLT_MAX ? 0.f : exp2f(m - M);
+    L += ws_ml[slot * 2 + 1] * w;
+    const float* src = ws_o + slot * HD + lane * per;
+    for (int i = 0; i < per; ++i) acc[i] += src[i] * w;
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  f16* dst = out + static_cast<std::int64_t>(c.row0 + r) * H * HD + h * HD + lane * per;
+  for (int i = 0; i < per; ++i) dst[i] = __float2half_rn(acc[i] * inv);
+}
+
+// Tensor maps are cached per (base, extent, geometry): executors created later
+// may reuse a freed buffer address with a different shape.
+const CUtensorMap& cached_tmap(const void* base, std::int64_t inner, std::int64_t rows, int box_rows) {
+  struct Key {
+    const void* p;
+    std::int64_t inner, rows;
+    int box;
+    bool operator==(const Key& o) const { return p == o.p && inner == o.inner && rows == o.rows && box == o.box; }
+  };
+  struct Hash {
+    std::size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.p) ^ (static_cast<std::size_t>(k.inner) << 20) ^
+             (static_cast<std::size_t>(k.rows) * 0x9E3779B97F4A7C15ULL) ^ static_cast<std::size_t>(k.box);
+    }
+  };
+  static std::mutex mu;
+  static std::unordered_map<Key, CUtensorMap, Hash> cache;
+  std::lock_guard<std::mutex> g(mu);
+  const Key key{base, inner, rows, box_rows};
+  auto it = cache.find(key);
+  if (it == cache.end()) it = cache.emplace(key, make_tmap_2d(base, inner, rows, inner * 2, 64, box_rows)).first;
+  return it->second;
+}
+
+const CUtensorMap& q_map(const f16* qkv, int rows, int D) { return cached_tmap(qkv, 3LL * D, rows, 128); }
+
+const CUtensorMap& kv_map(const KvGeom& g) {
+  const std::int64_t rows = static_cast<std::int64_t>(g.layers) * g.num_blocks * 2 * g.heads * kBlockTokens;
+  if (rows >= (1LL << 31)) throw DeviceError("KV pool too large for 32-bit TMA row coordinates");
+  return cached_tmap(g.pool, g.head_dim, rows, kBlockTokens);
+}
+
+template <int HD>
+void launch_chunk_hd(const f16* qkv, int qkv_rows, const TileDesc* items, int n_items, const KvGeom& g, int layer,
+                     f16* out, float* ws_o, float* ws_ml, cudaStream_t s) {
+  using C = AttnCfg<HD>;
+  static bool configured = false;
+  if (!configured) {
+    IB2_CUDA(cudaFuncSetAttribute(chunk_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL));
+    configured = true;
+  }
+  const std::int64_t layer_row0 = static_cast<std::int64_t>(layer) * g.num_blocks * 2 * g.heads * kBlockTokens;
+  launch_pdl(chunk_attn_tc_kernel<HD>, dim3(n_items, g.heads), dim3(256), C::TOTAL, s, q_map(qkv, qkv_rows, g.heads * HD),
+             kv_map(g), items, g.table, g.max_lblocks, layer_row0, g.heads, out, ws_o, ws_ml);
+  IB2_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+int chunk_attention_key_tile(int head_dim) {
+  switch (head_dim) {
+    case 64: return AttnCfg<64>::BN;
+    case 128: return AttnCfg<128>::BN;
+    case 256: return AttnCfg<256>::BN;
+    default: throw DeviceError("unsupported head_dim");
+  }
+}
+
+void launch_chunk_attention(const f16* qkv, int qkv_rows, const TileDesc* items, int n_items,
+                            const CombineDesc* combines, int n_combines, const KvGeom& g, int layer, f16* out,
+                            float* ws_o, float* ws_ml, cudaStream_t s) {
+  if (n_items <= 0) return;
+  switch (g.head_dim) {
+    case 64: launch_chunk_hd<64>(qkv, qkv_rows, items, n_items, g, layer, out, ws_o, ws_ml, s); break;
+    case 128: launch_chunk_hd<128>(qkv, qkv_rows, items, n_items, g, layer, out, ws_o, ws_ml, s); break;
+    case 256: launch_chunk_hd<256>(qkv, qkv_rows, items, n_items, g, layer, out, ws_o, ws_ml, s); break;
+    default: throw DeviceError("unsupported head_dim");
+  }
+  if (n_combines > 0) {
+    launch_pdl(chunk_combine_kernel, dim3(n_combines, g.heads, kChunkTileRows / 8), dim3(256), 0, s, combines, g.heads,
+               g.head_dim, ws_o, ws_ml, out);
+    IB2_LAUNCH_CHECK();
+  }
+}
+
+}  // namespace ib2

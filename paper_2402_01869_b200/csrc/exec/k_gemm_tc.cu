@@ -206,22 +206,22 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
 }
 
 
-// ---- small-M path: swap-AB, persistent whole tiles or cluster K-split ------
+// ---- small-M path: swap-AB stream-K ------------------------------------------
 //
 // Decode-dominated iterations have M (tokens) of 8..256 while the N x K
 // weights are 17-134 MB per projection: the GEMM is a weight stream.  C^T =
 // W A^T puts 128 weight rows on the UMMA M side (TMEM lanes) and the tokens on
 // the UMMA N side (NT columns), so every weight byte is read exactly once.
 //
-// SPLIT == 1 (N/128 >= ~100 tiles: QKV, MLP-in, LM head): persistent, one
-//   CTA per SM owning a contiguous run of whole weight tiles; the TMA ring never
-//   drains between tiles and accumulators alternate between two TMEM buffers so
-//   the epilogue of tile i overlaps the MMAs of tile i+1.
-// SPLIT in {2,4} (few tiles: O and MLP-out, N = d_model): the K range of a
-//   tile is split over a thread-block cluster of SPLIT CTAs; each writes its
-//   fp32 partial tile to its own shared memory and rank 0 sums the partials
-//   over DSMEM (ld.shared::cluster) in rank order -- deterministic, no global
-//   workspace -- before the fused epilogue.
+// Stream-K: the tiles x k-blocks units of work are cut into gridDim.x equal
+// contiguous ranges, one per CTA (one CTA per SM), so every SM streams the
+// same number of weight bytes whatever N/128 is.  A range covers whole tiles
+// in its middle (epilogue straight from TMEM) and partial tiles at its ends:
+// those write an fp32 partial [NT][128] into the CTA's own workspace slot,
+// and the last CTA to finish a tile (atomic ticket) sums the tile's partials
+// in CTA order -- deterministic -- and runs the fused epilogue.  Accumulators
+// alternate between two TMEM buffers so the epilogue of one segment overlaps
+// the MMAs of the next; the TMA ring never drains between segments.
 
 template <int NT, int STAGES>
 struct SkSmem {
@@ -231,7 +231,6 @@ struct SkSmem {
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
   static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
-  static_assert(NT * BM * 4 <= BAR_OFF, "partial tile must fit in the stage ring");
 };
 
 __device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v) {
@@ -257,24 +256,25 @@ __device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v
   if (m < a.M && n < a.N) epi_one(a, m, n, v);
 }
 
-__device__ __forceinline__ void cluster_sync_all() {
-  __syncwarp();
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-__device__ __forceinline__ std::uint32_t tmem_ld16(std::uint32_t taddr, std::uint32_t* r) {
+__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-  return 0;
 }
 
-template <int NT, int STAGES, int SPLIT>
-__global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant__ CUtensorMap map_w,
-                                                           const __grid_constant__ CUtensorMap map_a, GemmArgs args) {
+// Unit range [start(c), start(c+1)) of CTA c; the CTA owning unit u.
+__device__ __forceinline__ std::int64_t sk_start(int c, std::int64_t U, int G) { return c * U / G; }
+__device__ __forceinline__ int sk_owner(std::int64_t u, std::int64_t U, int G) {
+  return static_cast<int>(((u + 1) * G - 1) / U);
+}
+
+template <int NT, int STAGES>
+__global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constant__ CUtensorMap map_w,
+                                                            const __grid_constant__ CUtensorMap map_a, GemmArgs args,
+                                                            float* __restrict__ ws, int* __restrict__ tickets) {
   using L = SkSmem<NT, STAGES>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -283,24 +283,13 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
   std::uint64_t* tfull = empty + STAGES;  // [2] MMA -> epilogue
   std::uint64_t* tempty = tfull + 2;      // [2] epilogue -> MMA
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles = (args.N + BM - 1) / BM, kblocks = args.K / BK;
-  // Segments of this CTA: whole tiles [t0, t1) (SPLIT == 1), or one k range of
-  // one tile (cluster split).
-  int t0, t1, kb0, kb1, rank = 0;
-  if (SPLIT == 1) {
-    t0 = static_cast<int>(static_cast<long long>(blockIdx.x) * tiles / gridDim.x);
-    t1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * tiles / gridDim.x);
-    kb0 = 0;
-    kb1 = kblocks;
-  } else {
-    rank = blockIdx.x % SPLIT;
-    t0 = blockIdx.x / SPLIT;
-    t1 = t0 + 1;
-    kb0 = rank * kblocks / SPLIT;
-    kb1 = (rank + 1) * kblocks / SPLIT;
-  }
+  const int kblocks = args.K / BK;
+  const std::int64_t U = static_cast<std::int64_t>((args.N + BM - 1) / BM) * kblocks;
+  const int G = gridDim.x, c = blockIdx.x;
+  const std::int64_t u0 = sk_start(c, U, G), u1 = sk_start(c + 1, U, G);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
@@ -330,7 +319,9 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
   if (warp == 0) {
     if (lane == 0) {
       int i = 0;
-      for (int t = t0; t < t1; ++t)
+      for (std::int64_t u = u0; u < u1;) {
+        const int t = static_cast<int>(u / kblocks), kb0 = static_cast<int>(u % kblocks);
+        const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int st = i % STAGES;
           if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
@@ -339,13 +330,17 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
           tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
           tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
         }
+        u += kb1 - kb0;
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(NT >> 3) << 17) |
                                       (static_cast<std::uint32_t>(BM >> 4) << 24);
-      int i = 0;
-      for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+      int i = 0, seg = 0;
+      for (std::int64_t u = u0; u < u1; ++seg) {
+        const int kb0 = static_cast<int>(u % kblocks);
+        const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -374,68 +369,71 @@ __global__ void __launch_bounds__(256, 1) tc_skinny_kernel(const __grid_constant
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          su32(&tfull[buf]))
                      : "memory");
+        u += kb1 - kb0;
       }
     }
   } else if (warp >= 4) {
     const int q = warp - 4, row = q * 32 + lane;
-    for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+    const int mcols = min(args.M, NT);
+    int seg = 0;
+    for (std::int64_t u = u0; u < u1; ++seg) {
+      const int t = static_cast<int>(u / kblocks), kb0 = static_cast<int>(u % kblocks);
+      const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
+      u += kb1 - kb0;
       const int buf = seg & 1;
       const int n = t * BM + row;
       mbar_wait(&tfull[buf], (seg / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      float* part = reinterpret_cast<float*>(smem);  // stage ring is idle once the MMAs completed
+      const bool whole = kb0 == 0 && kb1 == kblocks;
+      // Partial segments go to slot 0 (the CTA's first tile) or 1 (its last).
+      float* part = ws + ((static_cast<std::int64_t>(c) * 2 + (seg == 0 ? 0 : 1)) * NT) * BM;
 #pragma unroll 1
-      for (int c = 0; c < NT; c += 16) {
-        if (c >= args.M) break;
+      for (int cc = 0; cc < mcols; cc += 16) {
         std::uint32_t r[16];
-        tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
+        tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + cc, r);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float v = __uint_as_float(r[j]);
-          if (SPLIT == 1) epi_row(args, n, c + j, v, lane);
-          else part[(c + j) * BM + row] = v;
+          if (whole) epi_row(args, n, cc + j, v, lane);
+          else if (cc + j < mcols) part[(cc + j) * BM + row] = v;
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[buf])) : "memory");
-    }
-  }
-  if (SPLIT > 1) {
-    // Partials sit in every CTA's shared memory.  Rank r reduces token
-    // columns [r*M/SPLIT, (r+1)*M/SPLIT) over DSMEM, always summing ranks in
-    // order 0..SPLIT-1 (deterministic), then runs the fused epilogue.
-    cluster_sync_all();
-    if (warp >= 4) {
-      const int row = (warp - 4) * 32 + lane, n = t0 * BM + row;
-      const std::uint32_t local = su32(smem);
-      std::uint32_t peer[SPLIT];
+      if (whole) continue;
+      // Ticket: the last of the tile's CTAs reduces.
+      const int c_first = sk_owner(static_cast<std::int64_t>(t) * kblocks, U, G);
+      const int c_last = sk_owner(static_cast<std::int64_t>(t) * kblocks + kblocks - 1, U, G);
+      __threadfence();
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (row == 0) {
+        const int prev = atomicAdd(&tickets[t], 1);
+        const bool last = prev == c_last - c_first;
+        if (last) tickets[t] = 0;  // ready for the next launch
+        *last_flag = last ? 1 : 0;
+      }
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (!*last_flag) continue;
+      __threadfence();
+      for (int m0 = 0; m0 < mcols; m0 += 16) {
+        float acc[16];
 #pragma unroll
-      for (int r = 0; r < SPLIT; ++r)
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer[r]) : "r"(local), "r"(r));
-      const int m_lo = rank * args.M / SPLIT, m_hi = (rank + 1) * args.M / SPLIT;
-      for (int m0 = m_lo; m0 < m_hi; m0 += 16) {
-        float x[SPLIT][16];
+        for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+        for (int o = c_first; o <= c_last; ++o) {
+          // CTA o's segment of tile t is its first (slot 0) unless tile t is
+          // not where o's range starts.
+          const int slot = (sk_start(o, U, G) / kblocks == t) ? 0 : 1;
+          const float* src = ws + ((static_cast<std::int64_t>(o) * 2 + slot) * NT) * BM;
 #pragma unroll
-        for (int r = 0; r < SPLIT; ++r)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            x[r][j] = 0.f;
-            if (m0 + j < m_hi)
-              asm volatile("ld.shared::cluster.f32 %0, [%1];\n"
-                           : "=f"(x[r][j])
-                           : "r"(peer[r] + static_cast<std::uint32_t>(((m0 + j) * BM + row) * 4)));
-          }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float v = 0.f;
-#pragma unroll
-          for (int r = 0; r < SPLIT; ++r) v += x[r][j];
-          if (m0 + j < m_hi) epi_row(args, n, m0 + j, v, lane);
+          for (int j = 0; j < 16; ++j)
+            if (m0 + j < mcols) acc[j] += __ldcg(src + (m0 + j) * BM + row);
         }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (m0 + j < mcols) epi_row(args, n, m0 + j, acc[j], lane);
       }
     }
-    cluster_sync_all();  // peers' shared memory stays alive until every rank is done
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
@@ -523,45 +521,49 @@ void launch_tc(const GemmArgs& a, cudaStream_t s) {
 
 int g_sms = 0;
 
-template <int NT, int STAGES, int SPLIT>
-void launch_skinny(const GemmArgs& a, int ctas, cudaStream_t s) {
-  using L = SkSmem<NT, STAGES>;
-  static bool configured = false;
-  if (!configured) {
-    IB2_CUDA(cudaFuncSetAttribute(tc_skinny_kernel<NT, STAGES, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  L::TOTAL));
-    configured = true;
+// Stream-K workspace: 2 partial slots of [256][128] fp32 per CTA, and one
+// ticket per weight tile (reset by the tile's reducer), per device.
+struct StreamKWs {
+  float* ws = nullptr;
+  int* tickets = nullptr;
+  int tiles = 0;
+};
+StreamKWs& streamk_ws(int tiles) {
+  static std::mutex mu;
+  static StreamKWs per_dev[16];
+  int dev = 0;
+  IB2_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  StreamKWs& w = per_dev[dev & 15];
+  if (!w.ws) IB2_CUDA(cudaMalloc(&w.ws, static_cast<std::size_t>(g_sms) * 2 * 256 * BM * sizeof(float)));
+  if (tiles > w.tiles) {
+    if (w.tickets) IB2_CUDA(cudaFree(w.tickets));
+    const int n = std::max(tiles, 1024);
+    IB2_CUDA(cudaMalloc(&w.tickets, n * sizeof(int)));
+    IB2_CUDA(cudaMemset(w.tickets, 0, n * sizeof(int)));
+    w.tiles = n;
   }
-  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
-  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
-  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = L::TOTAL;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = SPLIT;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_skinny_kernel<NT, STAGES, SPLIT>, mw, ma, a));
+  return w;
 }
 
 template <int NT, int STAGES>
-void launch_skinny_nt(const GemmArgs& a, cudaStream_t s) {
+void launch_skinny(const GemmArgs& a, cudaStream_t s) {
+  using L = SkSmem<NT, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    IB2_CUDA(cudaFuncSetAttribute(tc_streamk_kernel<NT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  L::TOTAL));
+    configured = true;
+  }
   const int tiles = static_cast<int>((a.N + BM - 1) / BM), kblocks = a.K / BK;
-  // Enough weight tiles (>= 2/3 of the SMs): persistent whole tiles.  Few
-  // tiles: split K over a cluster of 4/3/2 CTAs per tile, one wave.
-  if (tiles * 3 >= g_sms * 2 || kblocks < 16) launch_skinny<NT, STAGES, 1>(a, std::min(g_sms, tiles), s);
-  else if (tiles * 4 <= g_sms) launch_skinny<NT, STAGES, 4>(a, tiles * 4, s);
-  else if (tiles * 3 <= g_sms) launch_skinny<NT, STAGES, 3>(a, tiles * 3, s);
-  else if (tiles * 2 <= g_sms) launch_skinny<NT, STAGES, 2>(a, tiles * 2, s);
-  else launch_skinny<NT, STAGES, 1>(a, std::min(g_sms, tiles), s);
+  const std::int64_t units = static_cast<std::int64_t>(tiles) * kblocks;
+  // One CTA per SM, each streaming >= 4 k-blocks (64 KB of weights).
+  const int ctas = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g_sms, units / 4)));
+  StreamKWs& w = streamk_ws(tiles);
+  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
+  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
+  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
+  launch_pdl(tc_streamk_kernel<NT, STAGES>, dim3(ctas), dim3(256), L::TOTAL, s, mw, ma, a, w.ws, w.tickets);
 }
 
 bool skinny_ok(const GemmArgs& a) {
@@ -575,16 +577,30 @@ void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
     IB2_CUDA(cudaGetDevice(&dev));
     IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  if (a.M <= 16) launch_skinny_nt<16, 10>(a, s);
-  else if (a.M <= 32) launch_skinny_nt<32, 9>(a, s);
-  else if (a.M <= 64) launch_skinny_nt<64, 8>(a, s);
-  else if (a.M <= 128) launch_skinny_nt<128, 6>(a, s);
-  else launch_skinny_nt<256, 4>(a, s);
+  if (a.M <= 16) launch_skinny<16, 10>(a, s);
+  else if (a.M <= 32) launch_skinny<32, 9>(a, s);
+  else if (a.M <= 64) launch_skinny<64, 8>(a, s);
+  else if (a.M <= 128) launch_skinny<128, 6>(a, s);
+  else launch_skinny<256, 4>(a, s);
 }
 
 }  // namespace
 
 void set_gemm_activation_rows(std::int64_t rows) { g_a_rows_capacity = rows; }
+
+CUtensorMap make_tmap_2d(const void* base, std::int64_t inner, std::int64_t rows, std::int64_t row_stride_bytes,
+                         int box_inner, int box_rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_stride_bytes)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw DeviceError("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+  return m;
+}
 
 bool gemm_uses_tcgen05() { return true; }
 

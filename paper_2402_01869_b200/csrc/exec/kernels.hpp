@@ -4,6 +4,8 @@
 // K7 swap gather/scatter, K8 block tables, K9 embeddings).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace ib2 {
@@ -44,9 +46,17 @@ void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const Row
 
 // K2: tiled causal attention over the paged prefix for chunk rows, split-KV
 // items + combine pass for tiles whose keys were split.
-void launch_chunk_attention(const f16* qkv, const TileDesc* tiles, int n_tiles, const CombineDesc* combines,
-                            int n_combines, const KvGeom& g, int layer, f16* out, float* ws_o, float* ws_ml,
-                            cudaStream_t s);
+// qkv_rows: row capacity of the qkv activation buffer (TMA bounds).
+void launch_chunk_attention(const f16* qkv, int qkv_rows, const TileDesc* items, int n_items,
+                            const CombineDesc* combines, int n_combines, const KvGeom& g, int layer, f16* out,
+                            float* ws_o, float* ws_ml, cudaStream_t s);
+// Keys per K2 tile for a head dim (split-KV ranges are aligned to it).
+int chunk_attention_key_tile(int head_dim);
+
+// 2-D f16 TMA descriptor over [rows][inner] (row stride in bytes), box
+// box_inner x box_rows, 128-byte swizzle.
+CUtensorMap make_tmap_2d(const void* base, std::int64_t inner, std::int64_t rows, std::int64_t row_stride_bytes,
+                         int box_inner, int box_rows);
 
 // K3: projection GEMM with fused epilogue.
 void launch_gemm(const GemmArgs& a, cudaStream_t s);
