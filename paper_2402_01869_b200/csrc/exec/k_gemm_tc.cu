@@ -17,6 +17,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <unordered_map>
@@ -206,31 +207,40 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__
 }
 
 
-// ---- small-M path: swap-AB stream-K ------------------------------------------
+// ---- small-M path: swap-AB, cluster split-K ----------------------------------
 //
 // Decode-dominated iterations have M (tokens) of 8..256 while the N x K
 // weights are 17-134 MB per projection: the GEMM is a weight stream.  C^T =
 // W A^T puts 128 weight rows on the UMMA M side (TMEM lanes) and the tokens on
 // the UMMA N side (NT columns), so every weight byte is read exactly once.
 //
-// Stream-K: the tiles x k-blocks units of work are cut into gridDim.x equal
-// contiguous ranges, one per CTA (one CTA per SM), so every SM streams the
-// same number of weight bytes whatever N/128 is.  A range covers whole tiles
-// in its middle (epilogue straight from TMEM) and partial tiles at its ends:
-// those write an fp32 partial [NT][128] into the CTA's own workspace slot,
-// and the last CTA to finish a tile (atomic ticket) sums the tile's partials
-// in CTA order -- deterministic -- and runs the fused epilogue.  Accumulators
-// alternate between two TMEM buffers so the epilogue of one segment overlaps
-// the MMAs of the next; the TMA ring never drains between segments.
+// Work split so every SM streams about the same number of bytes: a cluster of
+// S CTAs owns a contiguous run of T weight tiles and CTA rank r streams the
+// k-slice r of each of them (S = 1: whole tiles).  Accumulators alternate
+// between two TMEM buffers, so a tile's epilogue overlaps the next tile's
+// MMAs and the TMA ring never drains.  With S > 1 each rank drops its fp32
+// partial tile into one of two shared-memory slots, signals every rank's
+// `ready` mbarrier over DSMEM, and rank r sums token columns
+// [r*M/S, (r+1)*M/S) of all S partials in rank order (ld.shared::cluster;
+// deterministic, no global workspace, no atomics) before the fused epilogue;
+// `consumed` mbarriers hand the slot back.  Only the epilogue warps take part,
+// so the weight stream never waits for the reduction.
 
 template <int NT, int STAGES>
 struct SkSmem {
   static constexpr int A_BYTES = BM * BK * 2;  // weights tile
   static constexpr int B_BYTES = NT * BK * 2;  // tokens tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  // fp32 partial-tile slots next to the ring: two for NT <= 64 (a tile's
+  // reduction overlaps the next tile's), one for NT = 128, none for 256.
+  static constexpr int PART_SLOTS = NT <= 64 ? 2 : (NT == 128 ? 1 : 0);
+  static constexpr bool SPLIT_OK = PART_SLOTS > 0;
+  static constexpr int PART_BYTES = NT * BM * 4;  // one fp32 partial tile
+  static constexpr int PART_OFF = STAGES * STAGE_BYTES;
+  static constexpr int BAR_OFF = PART_OFF + PART_SLOTS * PART_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 8) * 8 + 16 + 1024;
   static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
+  static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
 __device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v) {
@@ -256,6 +266,49 @@ __device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v
   if (m < a.M && n < a.N) epi_one(a, m, n, v);
 }
 
+// Epilogue of weight row n (this lane) for tokens m0..m0+15: every global
+// load is issued before any store so the 16 residual read-modify-writes
+// overlap instead of paying one memory latency each.
+__device__ __forceinline__ void epi_rows16(const GemmArgs& a, int n, int m0, const float* v, int lane) {
+  if (a.epi == Epi::SwiGluF16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float up = __shfl_down_sync(0xffffffffu, v[j], 1);
+      if (!(lane & 1) && m0 + j < a.M && n < a.N)
+        a.out[static_cast<std::int64_t>(m0 + j) * a.ldo + n / 2] = __float2half_rn(silu(v[j]) * up);
+    }
+    return;
+  }
+  if (n >= a.N) return;
+  const float b = a.bias ? __half2float(a.bias[n]) : 0.f;
+  switch (a.epi) {
+    case Epi::StoreF16:
+    case Epi::GeluF16:
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < a.M) {
+          const float x = v[j] + b;
+          a.out[static_cast<std::int64_t>(m0 + j) * a.ldo + n] = __float2half_rn(a.epi == Epi::GeluF16 ? gelu_tanh(x) : x);
+        }
+      break;
+    case Epi::ResidAdd: {
+      float old[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) old[j] = m0 + j < a.M ? a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < a.M) a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] = old[j] + (v[j] + b);
+      break;
+    }
+    case Epi::StoreF32:
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < a.M) a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] = v[j] + b;
+      break;
+    default: break;
+  }
+}
+
 __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
@@ -265,16 +318,35 @@ __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t* r)
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-// Unit range [start(c), start(c+1)) of CTA c; the CTA owning unit u.
-__device__ __forceinline__ std::int64_t sk_start(int c, std::int64_t U, int G) { return c * U / G; }
-__device__ __forceinline__ int sk_owner(std::int64_t u, std::int64_t U, int G) {
-  return static_cast<int>(((u + 1) * G - 1) / U);
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t map_to_rank(std::uint32_t local, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void arrive_remote(std::uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void wait_cluster(std::uint64_t* b, std::uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
 }
 
 template <int NT, int STAGES>
-__global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constant__ CUtensorMap map_w,
-                                                            const __grid_constant__ CUtensorMap map_a, GemmArgs args,
-                                                            float* __restrict__ ws, int* __restrict__ tickets) {
+__global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant__ CUtensorMap map_w,
+                                                           const __grid_constant__ CUtensorMap map_a, GemmArgs args,
+                                                           int S) {
   using L = SkSmem<NT, STAGES>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -282,14 +354,18 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
   std::uint64_t* empty = full + STAGES;
   std::uint64_t* tfull = empty + STAGES;  // [2] MMA -> epilogue
   std::uint64_t* tempty = tfull + 2;      // [2] epilogue -> MMA
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
-  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  std::uint64_t* ready = tempty + 2;      // [2] all ranks' partials of a slot written
+  std::uint64_t* consumed = ready + 2;    // [2] all ranks done reading a slot
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(consumed + 2);
+  float* parts = reinterpret_cast<float*>(smem + L::PART_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kblocks = args.K / BK;
-  const std::int64_t U = static_cast<std::int64_t>((args.N + BM - 1) / BM) * kblocks;
-  const int G = gridDim.x, c = blockIdx.x;
-  const std::int64_t u0 = sk_start(c, U, G), u1 = sk_start(c + 1, U, G);
+  const int tiles = (args.N + BM - 1) / BM, kblocks = args.K / BK;
+  const int rank = S > 1 ? static_cast<int>(cluster_rank()) : 0;
+  const int n_clusters = gridDim.x / S, cid = blockIdx.x / S;
+  const int t0 = static_cast<int>(static_cast<long long>(cid) * tiles / n_clusters);
+  const int t1 = static_cast<int>(static_cast<long long>(cid + 1) * tiles / n_clusters);
+  const int kb0 = rank * kblocks / S, kb1 = (rank + 1) * kblocks / S;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
@@ -301,6 +377,8 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+      mbar_init(&ready[i], 4 * S);
+      mbar_init(&consumed[i], 4 * S);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -311,6 +389,9 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (S > 1) {  // peers' barriers are initialised before anyone signals them
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
   pdl_trigger();
@@ -319,9 +400,7 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
   if (warp == 0) {
     if (lane == 0) {
       int i = 0;
-      for (std::int64_t u = u0; u < u1;) {
-        const int t = static_cast<int>(u / kblocks), kb0 = static_cast<int>(u % kblocks);
-        const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
+      for (int t = t0; t < t1; ++t)
         for (int kb = kb0; kb < kb1; ++kb, ++i) {
           const int st = i % STAGES;
           if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
@@ -330,17 +409,13 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
           tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
           tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
         }
-        u += kb1 - kb0;
-      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(NT >> 3) << 17) |
                                       (static_cast<std::uint32_t>(BM >> 4) << 24);
-      int i = 0, seg = 0;
-      for (std::int64_t u = u0; u < u1; ++seg) {
-        const int kb0 = static_cast<int>(u % kblocks);
-        const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
+      int i = 0;
+      for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -369,74 +444,75 @@ __global__ void __launch_bounds__(256, 1) tc_streamk_kernel(const __grid_constan
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          su32(&tfull[buf]))
                      : "memory");
-        u += kb1 - kb0;
       }
     }
   } else if (warp >= 4) {
     const int q = warp - 4, row = q * 32 + lane;
     const int mcols = min(args.M, NT);
-    int seg = 0;
-    for (std::int64_t u = u0; u < u1; ++seg) {
-      const int t = static_cast<int>(u / kblocks), kb0 = static_cast<int>(u % kblocks);
-      const int kb1 = static_cast<int>(kblocks < kb0 + (u1 - u) ? kblocks : kb0 + (u1 - u));
-      u += kb1 - kb0;
+    const int m_lo = rank * mcols / S, m_hi = (rank + 1) * mcols / S;
+    for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
       const int buf = seg & 1;
       const int n = t * BM + row;
       mbar_wait(&tfull[buf], (seg / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const bool whole = kb0 == 0 && kb1 == kblocks;
-      // Partial segments go to slot 0 (the CTA's first tile) or 1 (its last).
-      float* part = ws + ((static_cast<std::int64_t>(c) * 2 + (seg == 0 ? 0 : 1)) * NT) * BM;
+      constexpr int NS = L::PART_SLOTS > 0 ? L::PART_SLOTS : 1;
+      const int slot = seg % NS;
+      float* part = parts + slot * (NT * BM);
+      if (S > 1 && seg >= NS) wait_cluster(&consumed[slot], ((seg / NS) - 1) & 1);
 #pragma unroll 1
       for (int cc = 0; cc < mcols; cc += 16) {
         std::uint32_t r[16];
         tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + cc, r);
+        float v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float v = __uint_as_float(r[j]);
-          if (whole) epi_row(args, n, cc + j, v, lane);
-          else if (cc + j < mcols) part[(cc + j) * BM + row] = v;
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+        if (S == 1) {
+          epi_rows16(args, n, cc, v, lane);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) part[(cc + j) * BM + row] = v[j];
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[buf])) : "memory");
-      if (whole) continue;
-      // Ticket: the last of the tile's CTAs reduces.
-      const int c_first = sk_owner(static_cast<std::int64_t>(t) * kblocks, U, G);
-      const int c_last = sk_owner(static_cast<std::int64_t>(t) * kblocks + kblocks - 1, U, G);
-      __threadfence();
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (row == 0) {
-        const int prev = atomicAdd(&tickets[t], 1);
-        const bool last = prev == c_last - c_first;
-        if (last) tickets[t] = 0;  // ready for the next launch
-        *last_flag = last ? 1 : 0;
-      }
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (!*last_flag) continue;
-      __threadfence();
-      for (int m0 = 0; m0 < mcols; m0 += 16) {
+      if (S == 1) continue;
+      // Partials of this slot -> every rank; then reduce this rank's columns.
+      if (lane < S) arrive_remote(map_to_rank(su32(&ready[slot]), lane));
+      wait_cluster(&ready[slot], (seg / NS) & 1);
+      const std::uint32_t local = su32(part) + row * 4;
+      for (int m0 = m_lo; m0 < m_hi; m0 += 16) {
         float acc[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-        for (int o = c_first; o <= c_last; ++o) {
-          // CTA o's segment of tile t is its first (slot 0) unless tile t is
-          // not where o's range starts.
-          const int slot = (sk_start(o, U, G) / kblocks == t) ? 0 : 1;
-          const float* src = ws + ((static_cast<std::int64_t>(o) * 2 + slot) * NT) * BM;
+        for (int rr = 0; rr < S; ++rr) {
+          const std::uint32_t peer = map_to_rank(local, rr);
+          float x[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (m0 + j < mcols) acc[j] += __ldcg(src + (m0 + j) * BM + row);
+          for (int j = 0; j < 16; ++j) {
+            x[j] = 0.f;
+            if (m0 + j < m_hi)
+              asm volatile("ld.shared::cluster.f32 %0, [%1];\n"
+                           : "=f"(x[j])
+                           : "r"(peer + static_cast<std::uint32_t>((m0 + j) * BM * 4)));
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += x[j];
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (m0 + j < mcols) epi_row(args, n, m0 + j, acc[j], lane);
+        // Columns past m_hi belong to the next rank: mask them out.
+        GemmArgs a2 = args;
+        a2.M = m_hi;
+        epi_rows16(a2, n, m0, acc, lane);
       }
+      __syncwarp();
+      if (lane < S) arrive_remote(map_to_rank(su32(&consumed[slot]), lane));
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
+  if (S > 1) {  // peers may still read this CTA's partial slots
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(L::TMEM_COLS));
@@ -521,29 +597,52 @@ void launch_tc(const GemmArgs& a, cudaStream_t s) {
 
 int g_sms = 0;
 
-// Stream-K workspace: 2 partial slots of [256][128] fp32 per CTA, and one
-// ticket per weight tile (reset by the tile's reducer), per device.
-struct StreamKWs {
-  float* ws = nullptr;
-  int* tickets = nullptr;
-  int tiles = 0;
+// Work split of a decode-sized GEMM: clusters of S CTAs (K-slices) over T
+// tiles each, chosen so the per-CTA weight stream ceil(tiles / clusters) *
+// kblocks / S is smallest (ties: smaller S), one CTA per SM.
+struct SplitPlan {
+  int S, clusters;
 };
-StreamKWs& streamk_ws(int tiles) {
+// Clusters are placed within a GPC, so fewer than SMs / S clusters of S
+// CTAs may be co-resident: ask the occupancy API (cached per kernel and S).
+template <typename Kernel>
+int max_clusters(Kernel kernel, int S, int smem) {
   static std::mutex mu;
-  static StreamKWs per_dev[16];
-  int dev = 0;
-  IB2_CUDA(cudaGetDevice(&dev));
+  static std::unordered_map<long long, int> cache;
+  const long long key = (reinterpret_cast<long long>(reinterpret_cast<const void*>(kernel)) << 4) ^ S;
   std::lock_guard<std::mutex> g(mu);
-  StreamKWs& w = per_dev[dev & 15];
-  if (!w.ws) IB2_CUDA(cudaMalloc(&w.ws, static_cast<std::size_t>(g_sms) * 2 * 256 * BM * sizeof(float)));
-  if (tiles > w.tiles) {
-    if (w.tickets) IB2_CUDA(cudaFree(w.tickets));
-    const int n = std::max(tiles, 1024);
-    IB2_CUDA(cudaMalloc(&w.tickets, n * sizeof(int)));
-    IB2_CUDA(cudaMemset(w.tickets, 0, n * sizeof(int)));
-    w.tiles = n;
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g_sms / S * S);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kernel, &cfg) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = g_sms / S;
   }
-  return w;
+  cache.emplace(key, n);
+  return n;
+}
+
+// Many tiles (more than fit as 2-CTA clusters): whole tiles, one CTA per SM
+// (more CTAs than that do not raise the weight stream rate).  Few tiles: one
+// tile per cluster, the largest S <= 4 whose clusters are all co-resident.
+template <typename Kernel>
+SplitPlan plan_split(Kernel kernel, int smem, int tiles, int kblocks, bool split_ok) {
+  if (!split_ok || tiles > max_clusters(kernel, 2, smem)) return {1, std::min(g_sms, tiles)};
+  int S = 1;
+  for (int s = 2; s <= 4; ++s)
+    if (kblocks / s >= 4 && tiles <= max_clusters(kernel, s, smem)) S = s;
+  return {S, tiles};
 }
 
 template <int NT, int STAGES>
@@ -551,19 +650,35 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   using L = SkSmem<NT, STAGES>;
   static bool configured = false;
   if (!configured) {
-    IB2_CUDA(cudaFuncSetAttribute(tc_streamk_kernel<NT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  L::TOTAL));
+    IB2_CUDA(cudaFuncSetAttribute(tc_splitk_kernel<NT, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    IB2_CUDA(cudaFuncSetAttribute(tc_splitk_kernel<NT, STAGES>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
   const int tiles = static_cast<int>((a.N + BM - 1) / BM), kblocks = a.K / BK;
-  const std::int64_t units = static_cast<std::int64_t>(tiles) * kblocks;
-  // One CTA per SM, each streaming >= 4 k-blocks (64 KB of weights).
-  const int ctas = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g_sms, units / 4)));
-  StreamKWs& w = streamk_ws(tiles);
+  static const int force_s = getenv("IB2_SPLIT_S") ? atoi(getenv("IB2_SPLIT_S")) : 0;  // diagnostics
+  SplitPlan sp = plan_split(tc_splitk_kernel<NT, STAGES>, L::TOTAL, tiles, kblocks, L::SPLIT_OK);
+  if (force_s > 0 && L::SPLIT_OK)
+    sp = {force_s, std::max(1, std::min(max_clusters(tc_splitk_kernel<NT, STAGES>, force_s, L::TOTAL), tiles))};
+  static const bool verbose = getenv("IB2_SPLIT_VERBOSE") != nullptr;
+  if (verbose) fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d\n", a.N, a.K, a.M, sp.S, sp.clusters);
   const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
-  launch_pdl(tc_streamk_kernel<NT, STAGES>, dim3(ctas), dim3(256), L::TOTAL, s, mw, ma, a, w.ws, w.tickets);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sp.clusters * sp.S);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = sp.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_splitk_kernel<NT, STAGES>, mw, ma, a, sp.S));
 }
 
 bool skinny_ok(const GemmArgs& a) {
@@ -578,9 +693,9 @@ void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
     IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   if (a.M <= 16) launch_skinny<16, 10>(a, s);
-  else if (a.M <= 32) launch_skinny<32, 9>(a, s);
-  else if (a.M <= 64) launch_skinny<64, 8>(a, s);
-  else if (a.M <= 128) launch_skinny<128, 6>(a, s);
+  else if (a.M <= 32) launch_skinny<32, 8>(a, s);
+  else if (a.M <= 64) launch_skinny<64, 6>(a, s);
+  else if (a.M <= 128) launch_skinny<128, 5>(a, s);
   else launch_skinny<256, 4>(a, s);
 }
 
