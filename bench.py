@@ -108,7 +108,7 @@ def shard_trace(ib, world, rank, tmpdir):
 def gpu_pools(host_gb, gpu_blocks=0):
     blocks = gpu_blocks or int(COST["gpu_kv_capacity"] // (16 * GPTJ_M)) + 512
     return dict(gpu_blocks=blocks, host_bytes=int(host_gb * 1e9), max_requests=1024, max_rows=4096, timing=True,
-                stage_tokens=3328)
+                stage_tokens=1024, swap_slots=10)
 
 
 def cpu_forward_sample(plans, n_plans=3):

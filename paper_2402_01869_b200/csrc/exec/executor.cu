@@ -15,6 +15,7 @@
 // Swap copies are asynchronous cudaMemcpyAsync on a dedicated copy stream;
 // staging buffers are double-buffered and ordered with events.
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstring>
@@ -151,13 +152,35 @@ class Impl final : public B200Executor {
   // diagnostics: per-iteration start events on the compute stream + the
   // iteration's composition (rows, decode rows, chunk rows, swap-in, swap-out)
   bool trace_iters_ = false;
-  std::vector<cudaEvent_t> iter_ev_;
+  // per iteration: start, before forward, after forward (compute stream)
+  std::vector<std::array<cudaEvent_t, 3>> iter_ev_;
+  cudaEvent_t iter_mark(int which) {
+    cudaEvent_t e;
+    IB2_CUDA(cudaEventCreate(&e));
+    IB2_CUDA(cudaEventRecord(e, main_));
+    if (which == 0) iter_ev_.push_back({e, nullptr, nullptr});
+    else iter_ev_.back()[which] = e;
+    return e;
+  }
   std::vector<std::array<std::int64_t, 5>> iter_info_;
-  std::vector<double> iter_ms_;
+  std::vector<std::array<double, 3>> iter_ms_;  // preamble, forward, swap-out + post phase
+  // diagnostics: host seconds blocked per cause (plan ring, token ring, swap
+  // slot reuse, host pool full) and host seconds inside consume()
+  double host_block_s_[4] = {0, 0, 0, 0};
+  double host_consume_s_ = 0.0;
+  void sync_event(cudaEvent_t e, int cause) {
+    if (!trace_iters_) {
+      IB2_CUDA(cudaEventSynchronize(e));
+      return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    IB2_CUDA(cudaEventSynchronize(e));
+    host_block_s_[cause] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
 
   f16* weights_ = nullptr;
   std::int64_t gpu_blocks_ = 0;
-  int max_lb_ = 0, max_slots_ = 0, max_rows_ = 0, max_ctx_ = 0, hist_stride_ = 0;
+  int max_lb_ = 0, max_slots_ = 0, max_rows_ = 0, max_ctx_ = 0, hist_stride_ = 0, max_samples_ = 0;
   f16* pool_ = nullptr;
   std::int32_t *table_ = nullptr, *stack_ = nullptr, *top_ = nullptr, *err_ = nullptr, *hist_ = nullptr;
   float* rope_cs_ = nullptr;
@@ -166,7 +189,10 @@ class Impl final : public B200Executor {
   std::int32_t* out_tok_ = nullptr;
 
   // plan upload
-  static constexpr int kRing = 4;
+  // Plans in flight: the host may run this many iterations ahead of the GPU,
+  // which is what lets a swap-in's H2D start long before the compute that
+  // needs it.
+  static constexpr int kRing = 16;
   std::size_t plan_bytes_ = 0;
   unsigned char* plan_host_[kRing] = {};
   unsigned char* plan_dev_[kRing] = {};
@@ -196,9 +222,9 @@ class Impl final : public B200Executor {
     int buf, n_ops, tokens;
     std::vector<std::int64_t> requests;  // whose blocks the scatter fills
   };
-  static constexpr int kSwapBufs = 3;
   static constexpr int kMaxSwapOps = 4096;
-  SwapBuf in_[kSwapBufs], out_[kSwapBufs];
+  int swap_slots_ = 3;  // staging buffers per direction
+  std::vector<SwapBuf> in_, out_;
   int in_next_ = 0, out_next_ = 0;
   std::vector<PendingIn> pending_in_;
   std::int64_t stage_tokens_ = 0;
@@ -295,6 +321,7 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
     host_bytes_ = static_cast<std::size_t>(cpu / m_cost * static_cast<double>(M) * 1.25) + (64u << 20);
   }
   stage_tokens_ = pj.value("stage_tokens", 4096);
+  swap_slots_ = std::max(2, pj.value("swap_slots", 3));
   overlap_swaps_ = pj.value("overlap_swaps", true);
 
   // weights
@@ -346,11 +373,14 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   attn_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * D);
   hid_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * spec_.ffn);
   lmrows_ = dalloc<f16>(static_cast<std::size_t>(max_rows_) * D);
-  logits_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.vocab);
+  // Sampling rows and decode rows: at most one per live request.
+  const std::size_t max_samples = static_cast<std::size_t>(std::min(max_rows_, max_slots_));
+  max_samples_ = static_cast<int>(max_samples);
+  logits_ = dalloc<float>(max_samples * spec_.vocab);
   out_tok_ = dalloc<std::int32_t>(max_rows_);
   const int max_splits = (max_ctx_ + 255) / 256;
-  part_o_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * spec_.head_dim());
-  part_ml_ = dalloc<float>(static_cast<std::size_t>(max_rows_) * spec_.heads * max_splits * 2);
+  part_o_ = dalloc<float>(max_samples * spec_.heads * max_splits * spec_.head_dim());
+  part_ml_ = dalloc<float>(max_samples * spec_.heads * max_splits * 2);
   set_gemm_activation_rows(max_rows_);
   chunk_ws_o_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * spec_.head_dim());
   chunk_ws_ml_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * 2);
@@ -372,7 +402,12 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   // swap path
   IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool_), host_bytes_, cudaHostAllocDefault));
   arena_.reset(host_bytes_);
-  for (SwapBuf* b : {&in_[0], &in_[1], &in_[2], &out_[0], &out_[1], &out_[2]}) {
+  in_.resize(swap_slots_);
+  out_.resize(swap_slots_);
+  std::vector<SwapBuf*> all_bufs;
+  for (auto& b : in_) all_bufs.push_back(&b);
+  for (auto& b : out_) all_bufs.push_back(&b);
+  for (SwapBuf* b : all_bufs) {
     b->stage = dalloc<f16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
     b->desc_dev = dalloc<SwapDesc>(kMaxSwapOps);
     b->prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 1);
@@ -404,7 +439,10 @@ Impl::~Impl() {
   cudaEventDestroy(mark_[0]);
   cudaEventDestroy(mark_[1]);
   cudaFreeHost(host_pool_);
-  for (SwapBuf* b : {&in_[0], &in_[1], &in_[2], &out_[0], &out_[1], &out_[2]}) {
+  std::vector<SwapBuf*> all_bufs;
+  for (auto& b : in_) all_bufs.push_back(&b);
+  for (auto& b : out_) all_bufs.push_back(&b);
+  for (SwapBuf* b : all_bufs) {
     cudaFree(b->stage);
     cudaFree(b->desc_dev);
     cudaFree(b->prefix_dev);
@@ -505,7 +543,11 @@ void Impl::apply_ops(const isim_batch_plan& p, int phase, std::vector<std::int32
 }
 
 void Impl::retire_host_memory(bool force) {
-  if (force) IB2_CUDA(cudaStreamSynchronize(copy_in_));
+  if (force) {
+    const auto t0 = std::chrono::steady_clock::now();
+    IB2_CUDA(cudaStreamSynchronize(copy_in_));
+    host_block_s_[3] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
   std::size_t keep = 0;
   for (std::size_t i = 0; i < pending_release_.size(); ++i) {
     const PendingRelease& r = pending_release_[i];
@@ -608,13 +650,13 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     const int n_ops = static_cast<int>(last - first);
     SwapBuf& b = swap_in ? in_[in_next_] : out_[out_next_];
     const int bi = swap_in ? in_next_ : out_next_;
-    if (swap_in) in_next_ = (in_next_ + 1) % kSwapBufs;
-    else out_next_ = (out_next_ + 1) % kSwapBufs;
+    if (swap_in) in_next_ = (in_next_ + 1) % swap_slots_;
+    else out_next_ = (out_next_ + 1) % swap_slots_;
     if (swap_in) flush_swap_in_buffer(bi);  // recycle: its previous batch must be scattered first
     // The pinned descriptor arrays of this buffer were last uploaded
-    // kSwapBufs uses ago (swap-in: on copy_in_ before that batch's data;
+    // swap_slots_ uses ago (swap-in: on copy_in_ before that batch's data;
     // swap-out: on the compute stream before its gather).
-    IB2_CUDA(cudaEventSynchronize(swap_in ? b.copied : b.consumed));
+    sync_event(swap_in ? b.copied : b.consumed, 2);
     std::int64_t off = 0;
     b.prefix_host[0] = 0;
     for (int k = 0; k < n_ops; ++k) {
@@ -712,14 +754,15 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
 }
 
 void Impl::consume(const isim_batch_plan& p) {
+  const auto consume_t0 = std::chrono::steady_clock::now();
+  struct ConsumeTimer {
+    const std::chrono::steady_clock::time_point t0;
+    double& acc;
+    ~ConsumeTimer() { acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+  } consume_timer{consume_t0, host_consume_s_};
   IB2_CUDA(cudaSetDevice(dev_));
   retire_host_memory(false);
-  if (trace_iters_) {
-    cudaEvent_t e;
-    IB2_CUDA(cudaEventCreate(&e));
-    IB2_CUDA(cudaEventRecord(e, main_));
-    iter_ev_.push_back(e);
-  }
+  if (trace_iters_) iter_mark(0);
   const int D = spec_.d_model;
 
   // ---- host-side plan lowering ------------------------------------------------
@@ -748,6 +791,8 @@ void Impl::consume(const isim_batch_plan& p) {
   }
   const int n_rows = static_cast<int>(rows.size());
   if (n_rows > max_rows_) throw DeviceError("executor: batch exceeds max_rows");
+  if (static_cast<int>(samples.size()) > max_samples_ || static_cast<int>(drows.size()) > max_samples_)
+    throw DeviceError("executor: more sampling / decode rows than max_requests");
   // Split-KV for chunk tiles (one CTA per SM: K2 holds 512 TMEM columns):
   // key ranges of at most `per` keys, `per` ~ the whole (tile, head) key work
   // spread over the SMs, at least 512 keys, aligned to K2's key tile.
@@ -794,7 +839,7 @@ void Impl::consume(const isim_batch_plan& p) {
   // ---- upload -----------------------------------------------------------------
   const int k = ring_;
   ring_ = (ring_ + 1) % kRing;
-  IB2_CUDA(cudaEventSynchronize(plan_done_[k]));
+  sync_event(plan_done_[k], 0);
   unsigned char* h = plan_host_[k];
   unsigned char* d = plan_dev_[k];
   std::size_t off = 0;
@@ -825,6 +870,7 @@ void Impl::consume(const isim_batch_plan& p) {
 
   // ---- forward ------------------------------------------------------------------
   (void)D;
+  if (trace_iters_) iter_mark(1);
   if (n_rows > 0) {
     rows_dev_ = d_rows;
     drows_dev_ = d_drows;
@@ -839,13 +885,14 @@ void Impl::consume(const isim_batch_plan& p) {
     for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
     forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(items.size()), static_cast<int>(samples.size()));
     if (!samples.empty() && !record_) {
-      IB2_CUDA(cudaEventSynchronize(tok_done_[k]));
+      sync_event(tok_done_[k], 1);
       IB2_CUDA(cudaMemcpyAsync(tok_host_[k], out_tok_, samples.size() * 4, cudaMemcpyDeviceToHost, main_));
       IB2_CUDA(cudaEventRecord(tok_done_[k], main_));
       d2h_bytes_ += static_cast<std::int64_t>(samples.size()) * 4;
     }
   }
 
+  if (trace_iters_) iter_mark(2);
   // ---- post-phase: swap-out gather + D2H, then frees -----------------------------
   std::vector<SwapDesc> dummy_in;
   apply_ops(p, 1, frees1, allocs1, dummy_in, sw_out, released1);
@@ -857,7 +904,7 @@ void Impl::consume(const isim_batch_plan& p) {
   if (!frees1.empty()) {
     const int k2 = ring_;
     ring_ = (ring_ + 1) % kRing;
-    IB2_CUDA(cudaEventSynchronize(plan_done_[k2]));
+    sync_event(plan_done_[k2], 0);
     std::memcpy(plan_host_[k2], frees1.data(), frees1.size() * 4);
     IB2_CUDA(cudaMemcpyAsync(plan_dev_[k2], plan_host_[k2], frees1.size() * 4, cudaMemcpyHostToDevice, main_));
     h2d_bytes_ += static_cast<std::int64_t>(frees1.size()) * 4;
@@ -1014,11 +1061,13 @@ void Impl::sync() {
   swap_ev_bytes_.clear();
   if (trace_iters_ && iter_ev_.size() > 1) {
     for (std::size_t i = 0; i + 1 < iter_ev_.size(); ++i) {
-      float ms = 0.f;
-      IB2_CUDA(cudaEventElapsedTime(&ms, iter_ev_[i], iter_ev_[i + 1]));
-      iter_ms_.push_back(ms);
+      float pre = 0.f, fwd = 0.f, post = 0.f;
+      IB2_CUDA(cudaEventElapsedTime(&pre, iter_ev_[i][0], iter_ev_[i][1]));
+      IB2_CUDA(cudaEventElapsedTime(&fwd, iter_ev_[i][1], iter_ev_[i][2]));
+      IB2_CUDA(cudaEventElapsedTime(&post, iter_ev_[i][2], iter_ev_[i + 1][0]));
+      iter_ms_.push_back({pre, fwd, post});
+      for (cudaEvent_t e : iter_ev_[i]) cudaEventDestroy(e);
     }
-    for (std::size_t i = 0; i + 1 < iter_ev_.size(); ++i) cudaEventDestroy(iter_ev_[i]);
     iter_ev_.erase(iter_ev_.begin(), iter_ev_.end() - 1);
   }
 }
@@ -1078,6 +1127,8 @@ std::string Impl::stats_json() const {
   j["swap_ms"] = swap_ms_;
   j["swap_bytes_timed"] = swap_bytes_timed_;
   j["kv_bytes_per_token"] = spec_.kv_bytes_per_token();
+  j["host_consume_s"] = host_consume_s_;
+  j["host_block_s"] = {host_block_s_[0], host_block_s_[1], host_block_s_[2], host_block_s_[3]};
   if (trace_iters_) {
     j["iter_ms"] = iter_ms_;
     j["iter_info"] = iter_info_;

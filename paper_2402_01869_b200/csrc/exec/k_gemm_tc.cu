@@ -519,6 +519,265 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   }
 }
 
+// ---- large-M path: CTA-pair (cta_group::2) persistent GEMM --------------------
+//
+// Chunk iterations (prefill / recompute, M ~ 0.3k-2k rows) are tensor-core
+// bound.  A cluster of 2 CTAs on neighbouring SMs computes 256 x 256 output
+// tiles with tcgen05.mma.cta_group::2 (M = 256 split over the pair's TMEM, N =
+// 256): each CTA stages its 128 rows of A and its 128 rows of W per 64-wide k
+// block, so shared-memory traffic per SM is 32 KB per 128x256x64 MMA instead
+// of 48 KB.  Persistent over the tile list (M-fastest, so the pairs running
+// together share weight tiles through L2); accumulators alternate between two
+// 256-column TMEM buffers so a tile's epilogue (4 warps per CTA, 16-byte
+// vector stores, fused bias / GELU / SwiGLU / residual) overlaps the next
+// tile's MMAs.
+//   warp 0      TMA producer (both CTAs; completion counted on the leader's
+//               full barrier via .cta_group::2);
+//   warp 1      MMA issuer (leader CTA only); commits multicast to both CTAs;
+//   warp 2      TMEM allocator (cta_group::2, 512 columns);
+//   warps 4-7   epilogue (both CTAs, own 128 rows).
+
+constexpr int kPairStages = 6;
+struct PairSmem {
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = kPairStages * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * kPairStages + 4) * 8 + 16 + 1024;
+};
+
+__device__ __forceinline__ std::uint32_t cta_rank_in_cluster() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t mapa_rank(std::uint32_t local, std::uint32_t rank) {
+  std::uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, std::uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];\n" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// 16 consecutive output columns n0.. of row m (vector stores when aligned).
+__device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, float* v) {
+  if (m >= a.M || n0 >= a.N) return;
+  const bool full = n0 + 16 <= a.N;
+  if (a.bias && a.epi != Epi::SwiGluF16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (full || n0 + i < a.N) v[i] += __half2float(a.bias[n0 + i]);
+  }
+  switch (a.epi) {
+    case Epi::StoreF16:
+    case Epi::GeluF16: {
+      if (a.epi == Epi::GeluF16) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = gelu_tanh(v[i]);
+      }
+      f16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0;
+      if (full && (a.ldo % 8) == 0) {
+        uint4 w[2];
+        std::uint32_t* u = reinterpret_cast<std::uint32_t*>(w);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          u[i] = *reinterpret_cast<const std::uint32_t*>(&h);
+        }
+        reinterpret_cast<uint4*>(o)[0] = w[0];
+        reinterpret_cast<uint4*>(o)[1] = w[1];
+      } else {
+        for (int i = 0; i < 16 && n0 + i < a.N; ++i) o[i] = __float2half_rn(v[i]);
+      }
+      break;
+    }
+    case Epi::ResidAdd:
+    case Epi::StoreF32: {
+      float* o = a.outf + static_cast<std::int64_t>(m) * a.ldf + n0;
+      if (full && (a.ldf % 4) == 0) {
+        float4* o4 = reinterpret_cast<float4*>(o);
+        if (a.epi == Epi::ResidAdd) {
+          float4 r[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) r[i] = o4[i];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            o4[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1], r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      } else {
+        for (int i = 0; i < 16 && n0 + i < a.N; ++i) o[i] = a.epi == Epi::ResidAdd ? o[i] + v[i] : v[i];
+      }
+      break;
+    }
+    case Epi::SwiGluF16: {
+      f16* o = a.out + static_cast<std::int64_t>(m) * a.ldo + n0 / 2;
+      if (full && (a.ldo % 8) == 0) {
+        uint4 w;
+        std::uint32_t* u = reinterpret_cast<std::uint32_t*>(&w);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const __half2 h = __floats2half2_rn(silu(v[4 * i]) * v[4 * i + 1], silu(v[4 * i + 2]) * v[4 * i + 3]);
+          u[i] = *reinterpret_cast<const std::uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(o) = w;
+      } else {
+        for (int i = 0; i < 16 && n0 + i < a.N; i += 2) o[i / 2] = __float2half_rn(silu(v[i]) * v[i + 1]);
+      }
+      break;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                                                              const __grid_constant__ CUtensorMap map_w,
+                                                              GemmArgs args) {
+  using L = PairSmem;
+  constexpr int STAGES = kPairStages;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + L::BAR_OFF);
+  std::uint64_t* empty = full + STAGES;
+  std::uint64_t* tfull = empty + STAGES;  // [2] MMA -> epilogues (multicast)
+  std::uint64_t* tempty = tfull + 2;      // [2] epilogues of both CTAs -> MMA (leader's)
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const std::uint32_t rank = cta_rank_in_cluster();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int MT = (args.M + 255) / 256, NTL = (args.N + 255) / 256;
+  const int total = MT * NTL;
+  const int nk = args.K / BK;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const std::uint32_t tmem = *tmem_slot;
+  pdl_trigger();
+  pdl_wait();  // the prologue above overlapped the predecessor kernel
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const std::uint32_t full0 = mapa_rank(su32(full), 0);  // leader's full barriers
+      int i = 0;
+      for (int t = pair; t < total; t += npairs) {
+        const int mt = t % MT, ntl = t / MT;
+        const int arow = mt * 256 + static_cast<int>(rank) * 128;
+        const int wtile = ntl * 2 + static_cast<int>(rank);  // this CTA's 128-row weight tile
+        for (int kb = 0; kb < nk; ++kb, ++i) {
+          const int st = i % STAGES;
+          if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
+          if (leader) mbar_expect_tx(&full[st], 2 * L::STAGE_BYTES);
+          unsigned char* sa = smem + st * L::STAGE_BYTES;
+          const std::uint32_t bar = full0 + st * 8;
+          tma_load_2d_pair(sa, &map_a, bar, kb * BK, arow);
+          tma_load_2d_pair(sa + L::A_BYTES, &map_w, bar, 0, (wtile * nk + kb) * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(256 >> 3) << 17) |
+                                      (static_cast<std::uint32_t>(256 >> 4) << 24);
+      int i = 0, seg = 0;
+      for (int t = pair; t < total; t += npairs, ++seg) {
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const std::uint32_t acc_tmem = tmem + buf * 256;
+        for (int kb = 0; kb < nk; ++kb, ++i) {
+          const int st = i % STAGES;
+          mbar_wait(&full[st], (i / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const unsigned char* sa = smem + st * L::STAGE_BYTES;
+          const std::uint64_t da = smem_desc(sa), db = smem_desc(sa + L::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            const std::uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n"
+                ".reg .pred p;\n"
+                "setp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+                "}\n" ::"r"(acc_tmem),
+                "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                  su32(&empty[st])),
+              "h"(static_cast<unsigned short>(3))
+              : "memory");
+        }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                su32(&tfull[buf])),
+            "h"(static_cast<unsigned short>(3))
+            : "memory");
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const std::uint32_t tempty0 = mapa_rank(su32(tempty), 0);
+    int seg = 0;
+    for (int t = pair; t < total; t += npairs, ++seg) {
+      const int buf = seg & 1;
+      const int mt = t % MT, ntl = t / MT;
+      const int m = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      mbar_wait(&tfull[buf], (seg / 2) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 16) {
+        std::uint32_t r[16];
+        tmem_ld16(tmem + buf * 256 + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+        epi_cols16(args, m, ntl * 256 + c, v);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(tempty0 + buf * 8)
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
+  }
+}
+
 // ---- host side ----------------------------------------------------------------
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -596,6 +855,35 @@ void launch_tc(const GemmArgs& a, cudaStream_t s) {
 
 
 int g_sms = 0;
+
+void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
+  using L = PairSmem;
+  static bool configured = false;
+  if (!configured) {
+    IB2_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    configured = true;
+  }
+  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
+  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, 128);
+  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, 128);
+  const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  const int pairs = std::max(1, std::min(g_sms / 2, tiles));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel, ma, mw, a));
+}
 
 // Work split of a decode-sized GEMM: clusters of S CTAs (K-slices) over T
 // tiles each, chosen so the per-CTA weight stream ceil(tiles / clusters) *
@@ -732,7 +1020,14 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s) {
   // Small M is weight-bandwidth bound: narrow N tiles put more SMs on the
   // weight stream.  Large M uses wide tiles for operand reuse.
   const std::int64_t tiles128 = static_cast<std::int64_t>((a.N + 127) / 128) * ((a.M + BM - 1) / BM);
-  if (a.M > 512 && a.N >= 1024) launch_tc<256, 4>(a, s);
+  static const bool no_pair = getenv("IB2_NO_PAIR_GEMM") != nullptr;  // diagnostics: old 1-CTA kernel
+  if (!g_sms) {
+    int dev = 0;
+    IB2_CUDA(cudaGetDevice(&dev));
+    IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (!no_pair) launch_tc_pair(a, s);
+  else if (a.M > 512 && a.N >= 1024) launch_tc<256, 4>(a, s);
   else if (tiles128 >= 148) launch_tc<128, 6>(a, s);
   else launch_tc<64, 8>(a, s);
 }

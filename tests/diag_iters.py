@@ -1,6 +1,8 @@
 """Diagnostic (not collected): per-iteration device time of the C1 window by
-iteration type (decode-only / chunk / with swaps)."""
-import sys, json
+iteration type, split into preamble (swap-in scatters it waits for, block
+tables, swap-in issue), forward, and post phase (swap-out gather, frees) --
+plus how long the host spent inside consume() and blocked on events."""
+import sys, time
 sys.path.insert(0, "/root/repo")
 import numpy as np
 import bench
@@ -14,16 +16,25 @@ sess.step(ff)
 ex.sync()
 st0 = ex.stats()
 k0 = len(st0["iter_ms"])
+w0 = time.perf_counter()
 sess.step(n)
+w1 = time.perf_counter()
 ex.sync()
+w2 = time.perf_counter()
 st = ex.stats()
-ms = np.array(st["iter_ms"][k0:])
-info = np.array(st["iter_info"][k0 + 1:k0 + 1 + len(ms)])  # iter_ms[i] = start(i) -> start(i+1)
-ms = ms[:len(info)]
+print(f"host: step() returned after {1e3*(w1-w0):.0f} ms, sync waited {1e3*(w2-w1):.0f} ms; consume() host total "
+      f"{1e3*(st['host_consume_s']-st0['host_consume_s']):.0f} ms; blocked (plan ring, tok ring, swap slot, host pool) ms:",
+      [round(1e3*(a-b)) for a, b in zip(st['host_block_s'], st0['host_block_s'])])
+ph = np.array(st["iter_ms"][k0:])            # iteration k0.. : [pre, fwd, post]
+info = np.array(st["iter_info"][k0:k0 + len(ph)])
+ms = ph.sum(axis=1)
 rows, drows, crows, sin, sout = info.T
 def show(name, mask):
     if mask.sum():
-        print(f"{name:28s} n={mask.sum():5d} mean={ms[mask].mean():7.2f} ms  p50={np.median(ms[mask]):7.2f}  total={ms[mask].sum():8.1f} ms  rows~{rows[mask].mean():.0f} swap~{(sin+sout)[mask].mean():.0f}")
+        p = ph[mask].mean(axis=0)
+        print(f"{name:24s} n={mask.sum():4d} mean={ms[mask].mean():6.2f} p50={np.median(ms[mask]):6.2f} ms "
+              f"[pre {p[0]:5.2f} fwd {p[1]:5.2f} post {p[2]:5.2f}] rows~{rows[mask].mean():.0f} "
+              f"in~{sin[mask].mean():.0f} out~{sout[mask].mean():.0f}")
 print("total", ms.sum(), "ms over", len(ms), "iterations")
 show("decode-only, no swap", (crows == 0) & (sin + sout == 0))
 show("decode-only, swap", (crows == 0) & (sin + sout > 0))
@@ -33,3 +44,4 @@ show("chunk>256", crows > 256)
 show("swap-in only", (sin > 0) & (sout == 0))
 show("swap-out only", (sout > 0) & (sin == 0))
 show("both directions", (sin > 0) & (sout > 0))
+show("all", ms > -1)
