@@ -187,6 +187,7 @@ def run_b200(args):
                        k1_ms=s1["k1_ms"] - s0["k1_ms"], k1_bytes=s1["k1_bytes"] - s0["k1_bytes"],
                        k1_launches=s1["k1_timed_launches"] - s0["k1_timed_launches"],
                        swap_ms=s1["swap_ms"] - s0["swap_ms"], swap_bytes=s1["swap_bytes_timed"] - s0["swap_bytes_timed"],
+                       fwd_tok=s1["swap_in_forwarded_tokens"] - s0["swap_in_forwarded_tokens"],
                        launches=s1["kernel_launches"] - s0["kernel_launches"],
                        h2d=s1["h2d_bytes"] - s0["h2d_bytes"], d2h=s1["d2h_bytes"] - s0["d2h_bytes"])
     if dist:
@@ -199,7 +200,8 @@ def run_b200(args):
         return
     dev_s = max(g["dev_s"] for g in gathered)
     wall_s = max(g["wall_s"] for g in gathered)
-    tot = {k: sum(g[k] for g in gathered) for k in ("completed", "decode", "swapped", "launches", "h2d", "d2h")}
+    tot = {k: sum(g[k] for g in gathered) for k in ("completed", "decode", "swapped", "launches", "h2d", "d2h",
+                                                    "fwd_tok")}
     pk = peaks()
     k1_gbs = local_stats["k1_bytes"] / (local_stats["k1_ms"] / 1e3) / 1e9 if local_stats["k1_ms"] else None
     swap_gbs = local_stats["swap_bytes"] / (local_stats["swap_ms"] / 1e3) / 1e9 if local_stats["swap_ms"] else None
@@ -224,6 +226,7 @@ def run_b200(args):
         "completed_in_window": tot["completed"],
         "swap_gbs_achieved": swap_gbs,
         "swap_tokens_in_window": tot["swapped"],
+        "swap_in_forwarded_tokens": tot["fwd_tok"],
         "roofline": {"bound": "hbm", "kernel": "K1 paged decode attention (middle layer, every timed iteration)",
                      "achieved": k1_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": (k1_gbs / pk["hbm_gbs"]) if k1_gbs and pk.get("hbm_gbs") else None,

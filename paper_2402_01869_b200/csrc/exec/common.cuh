@@ -106,8 +106,8 @@ struct SwapDesc {
   std::int32_t slot;
   std::int32_t pos0;
   std::int32_t n;
-  std::int32_t pad;
-  std::int64_t stage_off;  // element offset of this op's [L][n][2D] slab
+  std::int32_t ld;         // tokens per layer of the staging slab (0: n)
+  std::int64_t stage_off;  // element offset of position pos0, layer 0, in a [L][ld][2D] slab
 };
 
 // Epilogue variants of the projection GEMMs.

@@ -91,6 +91,11 @@ struct Extent {
   std::size_t off;        // arena offset
   std::size_t bytes;
   std::int64_t d2h_seq;   // 1-based index of the D2H batch that wrote it
+  // The swap-out staging slot that held the extent's [L][n][2D] slab on the
+  // way out, valid while that slot's generation is unchanged.
+  int out_slot;
+  std::int64_t out_gen;
+  std::int64_t stage_off;
 };
 
 template <typename T>
@@ -164,6 +169,19 @@ class Impl final : public B200Executor {
   }
   std::vector<std::array<std::int64_t, 5>> iter_info_;
   std::vector<std::array<double, 3>> iter_ms_;  // preamble, forward, swap-out + post phase
+  // diagnostics: host/GPU timeline against a reference point taken in sync()
+  cudaEvent_t trace_ref_ = nullptr;
+  std::chrono::steady_clock::time_point trace_ref_host_;
+  std::vector<double> iter_host_ms_;  // host time consume() started (rel. ref)
+  std::vector<double> iter_lead_ms_;  // GPU start - host start of each iteration
+  struct SwapTrace {
+    std::int64_t iter;
+    int dir;  // 0 = in (H2D), 1 = out (D2H)
+    cudaEvent_t t0, t1;
+    double bytes;
+  };
+  std::vector<SwapTrace> swap_trace_pending_;
+  std::vector<std::array<double, 5>> swap_trace_;  // iter, dir, start, end (ms rel. ref), bytes
   // diagnostics: host seconds blocked per cause (plan ring, token ring, swap
   // slot reuse, host pool full) and host seconds inside consume()
   double host_block_s_[4] = {0, 0, 0, 0};
@@ -194,7 +212,8 @@ class Impl final : public B200Executor {
   // needs it.
   static constexpr int kRing = 16;
   std::size_t plan_bytes_ = 0;
-  unsigned char* plan_host_[kRing] = {};
+  unsigned char* plan_host_[kRing] = {};      // pinned, mapped
+  unsigned char* plan_host_dev_[kRing] = {};  // device view of plan_host_
   unsigned char* plan_dev_[kRing] = {};
   cudaEvent_t plan_done_[kRing] = {};
   int ring_ = 0;
@@ -226,6 +245,21 @@ class Impl final : public B200Executor {
   int swap_slots_ = 3;  // staging buffers per direction
   std::vector<SwapBuf> in_, out_;
   int in_next_ = 0, out_next_ = 0;
+  std::vector<std::int64_t> out_gen_;  // per swap-out slot: bumped when the slot is refilled
+  // Swap-ins whose bytes are still in a swap-out staging slot (a request whose
+  // API call returned before its swap-out slot was reused) are scattered from
+  // that slot on the compute stream -- the same bytes, no PCIe round trip.
+  struct FwdBuf {
+    SwapDesc* desc_host = nullptr;  // pinned, mapped
+    std::int32_t* prefix_host = nullptr;
+    SwapDesc* desc_dev = nullptr;
+    std::int32_t* prefix_dev = nullptr;
+    cudaEvent_t done = nullptr;
+  };
+  static constexpr int kFwdBufs = 4;
+  FwdBuf fwd_[kFwdBufs];
+  int fwd_next_ = 0;
+  std::int64_t swap_in_forwarded_tok_ = 0;
   std::vector<PendingIn> pending_in_;
   std::int64_t stage_tokens_ = 0;
   bool overlap_swaps_ = true;
@@ -239,7 +273,8 @@ class Impl final : public B200Executor {
   cudaEvent_t new_timing_event();
   // sampled ids streamed to pinned host memory every iteration (the result
   // a serving frontend would read)
-  std::int32_t* tok_host_[kRing] = {};
+  std::int32_t* tok_host_[kRing] = {};      // pinned, mapped: the argmax kernel stores the ids here
+  std::int32_t* tok_host_dev_[kRing] = {};
   cudaEvent_t tok_done_[kRing] = {};
   std::int64_t h2d_bytes_ = 0, d2h_bytes_ = 0;
   cudaEvent_t mark_[2] = {};
@@ -271,6 +306,13 @@ class Impl final : public B200Executor {
   int n_combines_ = 0;
   float *chunk_ws_o_ = nullptr, *chunk_ws_ml_ = nullptr;
   const std::int32_t* samples_dev_ = nullptr;
+  std::int32_t* tok_out_host_ = nullptr;
+  template <typename T>
+  static const void* mapped(const T* host) {
+    void* d = nullptr;
+    IB2_CUDA(cudaHostGetDevicePointer(&d, const_cast<T*>(host), 0));
+    return d;
+  }
   double k1_bytes_iter_ = 0.0;
   int max_pos1_ = 0;
 };
@@ -390,10 +432,13 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
                 static_cast<std::size_t>(kMaxChunkParts + max_rows_) * (sizeof(TileDesc) + sizeof(CombineDesc)) +
                 static_cast<std::size_t>(max_slots_) * max_lb_ * 4 * 3 + 4096;
   for (int i = 0; i < kRing; ++i) {
-    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[i]), plan_bytes_, cudaHostAllocDefault));
-    plan_dev_[i] = dalloc<unsigned char>(plan_bytes_);
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&plan_host_[i]), plan_bytes_ + 16, cudaHostAllocMapped));
+    IB2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&plan_host_dev_[i]), plan_host_[i], 0));
+    plan_dev_[i] = dalloc<unsigned char>(plan_bytes_ + 16);
     IB2_CUDA(cudaEventCreateWithFlags(&plan_done_[i], cudaEventDisableTiming));
-    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&tok_host_[i]), static_cast<std::size_t>(max_rows_) * 4, 0));
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&tok_host_[i]), static_cast<std::size_t>(max_rows_) * 4,
+                           cudaHostAllocMapped));
+    IB2_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&tok_host_dev_[i]), tok_host_[i], 0));
     IB2_CUDA(cudaEventCreateWithFlags(&tok_done_[i], cudaEventDisableTiming));
   }
   IB2_CUDA(cudaEventCreate(&mark_[0]));
@@ -409,12 +454,22 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   for (auto& b : out_) all_bufs.push_back(&b);
   for (SwapBuf* b : all_bufs) {
     b->stage = dalloc<f16>(static_cast<std::size_t>(stage_tokens_) * spec_.layers * 2 * D);
-    b->desc_dev = dalloc<SwapDesc>(kMaxSwapOps);
-    b->prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 1);
-    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->desc_host), kMaxSwapOps * sizeof(SwapDesc), 0));
-    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->prefix_host), (kMaxSwapOps + 1) * 4, 0));
+    b->desc_dev = dalloc<SwapDesc>(kMaxSwapOps + 1);
+    b->prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 8);
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->desc_host), (kMaxSwapOps + 1) * sizeof(SwapDesc),
+                           cudaHostAllocMapped));
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b->prefix_host), (kMaxSwapOps + 8) * 4, cudaHostAllocMapped));
     IB2_CUDA(cudaEventCreateWithFlags(&b->copied, cudaEventDisableTiming));
     IB2_CUDA(cudaEventCreateWithFlags(&b->consumed, cudaEventDisableTiming));
+  }
+  out_gen_.assign(swap_slots_, 0);
+  for (FwdBuf& f : fwd_) {
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.desc_host), (kMaxSwapOps + 1) * sizeof(SwapDesc),
+                           cudaHostAllocMapped));
+    IB2_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&f.prefix_host), (kMaxSwapOps + 8) * 4, cudaHostAllocMapped));
+    f.desc_dev = dalloc<SwapDesc>(kMaxSwapOps + 1);
+    f.prefix_dev = dalloc<std::int32_t>(kMaxSwapOps + 8);
+    IB2_CUDA(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
   }
   IB2_CUDA(cudaStreamSynchronize(main_));
 }
@@ -438,6 +493,13 @@ Impl::~Impl() {
   }
   cudaEventDestroy(mark_[0]);
   cudaEventDestroy(mark_[1]);
+  for (FwdBuf& f : fwd_) {
+    cudaFreeHost(f.desc_host);
+    cudaFreeHost(f.prefix_host);
+    cudaFree(f.desc_dev);
+    cudaFree(f.prefix_dev);
+    cudaEventDestroy(f.done);
+  }
   cudaFreeHost(host_pool_);
   std::vector<SwapBuf*> all_bufs;
   for (auto& b : in_) all_bufs.push_back(&b);
@@ -617,6 +679,8 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
   // Split ops at host-extent boundaries (swap-in) and at the staging size.
   std::vector<SwapDesc> ops;
   std::vector<std::pair<std::int64_t, std::size_t>> ext_of;  // (request, extent index)
+  std::vector<std::pair<int, SwapDesc>> fwd;                 // (swap-out slot, scatter descriptor)
+  std::vector<std::int64_t> fwd_reqs;
   for (std::size_t i = 0; i < in_ops.size(); ++i) {
     const SwapDesc& o = in_ops[i];
     if (!swap_in) {
@@ -636,10 +700,46 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
       std::size_t e = 0;
       while (e < exts.size() && !(exts[e].lo <= lo && lo < exts[e].hi)) ++e;
       if (e == exts.size()) throw DeviceError("executor: swap-in of positions not on the host");
-      const std::int64_t end = std::min({hi, exts[e].hi, lo + stage_tokens_});
+      Extent& x = exts[e];
+      if (x.out_slot >= 0 && out_gen_[x.out_slot] == x.out_gen) {
+        // Still in its swap-out staging slot: forward from there.
+        const std::int64_t end = std::min(hi, x.hi);
+        fwd.push_back({x.out_slot,
+                       SwapDesc{o.slot, static_cast<std::int32_t>(lo), static_cast<std::int32_t>(end - lo),
+                                static_cast<std::int32_t>(x.hi0 - x.lo0),
+                                x.stage_off + (lo - x.lo0) * 2 * D}});
+        x.lo = end;
+        fwd_reqs.push_back(req_of[i]);
+        swap_in_forwarded_tok_ += end - lo;
+        lo = end;
+        continue;
+      }
+      const std::int64_t end = std::min({hi, x.hi, lo + stage_tokens_});
       ops.push_back({o.slot, static_cast<std::int32_t>(lo), static_cast<std::int32_t>(end - lo), 0, 0});
       ext_of.push_back({req_of[i], e});
       lo = end;
+    }
+  }
+  if (!fwd.empty()) {
+    std::stable_sort(fwd.begin(), fwd.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (std::size_t g0 = 0; g0 < fwd.size();) {
+      std::size_t g1 = g0;
+      while (g1 < fwd.size() && fwd[g1].first == fwd[g0].first && g1 - g0 < kMaxSwapOps) ++g1;
+      FwdBuf& f = fwd_[fwd_next_];
+      fwd_next_ = (fwd_next_ + 1) % kFwdBufs;
+      sync_event(f.done, 2);
+      f.prefix_host[0] = 0;
+      const int n = static_cast<int>(g1 - g0);
+      for (int k = 0; k < n; ++k) {
+        f.desc_host[k] = fwd[g0 + k].second;
+        f.prefix_host[k + 1] = f.prefix_host[k] + f.desc_host[k].n;
+      }
+      launch_copy_from_host(f.desc_dev, mapped(f.desc_host), n * sizeof(SwapDesc), main_);
+      launch_copy_from_host(f.prefix_dev, mapped(f.prefix_host), (n + 1) * 4, main_);
+      launch_swap_copy(f.desc_dev, f.prefix_dev, n, f.prefix_host[n], geom(), out_[fwd[g0].first].stage, false, main_);
+      kernel_launches_ += 3;
+      IB2_CUDA(cudaEventRecord(f.done, main_));
+      g0 = g1;
     }
   }
   std::size_t first = 0;
@@ -652,6 +752,7 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     const int bi = swap_in ? in_next_ : out_next_;
     if (swap_in) in_next_ = (in_next_ + 1) % swap_slots_;
     else out_next_ = (out_next_ + 1) % swap_slots_;
+    if (!swap_in) ++out_gen_[bi];  // the slot's previous slabs are about to be overwritten
     if (swap_in) flush_swap_in_buffer(bi);  // recycle: its previous batch must be scattered first
     // The pinned descriptor arrays of this buffer were last uploaded
     // swap_slots_ uses ago (swap-in: on copy_in_ before that batch's data;
@@ -667,7 +768,7 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
     }
     const int tokens = b.prefix_host[n_ops];
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (timing_) {
+    if (timing_ || trace_iters_) {
       t0 = new_timing_event();
       t1 = new_timing_event();
     }
@@ -698,6 +799,7 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
         IB2_CUDA(cudaEventRecord(t1, copy_in_));
         swap_ev_pending_.push_back({t0, t1});
         swap_ev_bytes_.push_back(batch_bytes);
+        if (trace_iters_ && trace_ref_) swap_trace_pending_.push_back({iters_, 0, t0, t1, batch_bytes});
       }
       std::vector<std::int64_t> reqs;
       for (int k = 0; k < n_ops; ++k)
@@ -707,8 +809,9 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
       if (!overlap_swaps_) flush_swap_ins();
     } else {
       IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));  // previous D2H out of this staging done
-      IB2_CUDA(cudaMemcpyAsync(b.desc_dev, b.desc_host, n_ops * sizeof(SwapDesc), cudaMemcpyHostToDevice, main_));
-      IB2_CUDA(cudaMemcpyAsync(b.prefix_dev, b.prefix_host, (n_ops + 1) * 4, cudaMemcpyHostToDevice, main_));
+      launch_copy_from_host(b.desc_dev, mapped(b.desc_host), n_ops * sizeof(SwapDesc), main_);
+      launch_copy_from_host(b.prefix_dev, mapped(b.prefix_host), (n_ops + 1) * 4, main_);
+      kernel_launches_ += 2;
       launch_swap_copy(b.desc_dev, b.prefix_dev, n_ops, tokens, geom(), b.stage, true, main_);
       ++kernel_launches_;
       IB2_CUDA(cudaEventRecord(b.consumed, main_));
@@ -721,7 +824,7 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
                                  copy_));
         extents_[ext_of[first + k].first].push_back({b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n,
                                                      b.desc_host[k].pos0, b.desc_host[k].pos0 + b.desc_host[k].n, hoff,
-                                                     bytes, d2h_seq_ + 1});
+                                                     bytes, d2h_seq_ + 1, bi, out_gen_[bi], b.desc_host[k].stage_off});
       }
       IB2_CUDA(cudaEventRecord(b.copied, copy_));
       IB2_CUDA(cudaEventRecord(d2h_ring_[d2h_seq_ % kSeqRing], copy_));
@@ -730,6 +833,7 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
         IB2_CUDA(cudaEventRecord(t1, copy_));
         swap_ev_pending_.push_back({t0, t1});
         swap_ev_bytes_.push_back(batch_bytes);
+        if (trace_iters_ && trace_ref_) swap_trace_pending_.push_back({iters_, 1, t0, t1, batch_bytes});
       }
       if (!overlap_swaps_) IB2_CUDA(cudaStreamWaitEvent(main_, b.copied, 0));
     }
@@ -738,8 +842,12 @@ void Impl::run_swaps(const std::vector<SwapDesc>& in_ops, const std::vector<std:
   if (swap_in) {
     // Fully consumed extents return to the arena once the H2D copies reading
     // them have completed (the D2H stream may otherwise overwrite them).
+    std::vector<std::int64_t> reqs = fwd_reqs;
     for (const auto& [rid, idx] : ext_of) {
       (void)idx;
+      reqs.push_back(rid);
+    }
+    for (const std::int64_t rid : reqs) {
       auto& exts = extents_[rid];
       for (std::size_t e = 0; e < exts.size();) {
         if (exts[e].lo >= exts[e].hi) {
@@ -762,7 +870,11 @@ void Impl::consume(const isim_batch_plan& p) {
   } consume_timer{consume_t0, host_consume_s_};
   IB2_CUDA(cudaSetDevice(dev_));
   retire_host_memory(false);
-  if (trace_iters_) iter_mark(0);
+  if (trace_iters_) {
+    iter_mark(0);
+    iter_host_ms_.push_back(
+        trace_ref_ ? std::chrono::duration<double, std::milli>(consume_t0 - trace_ref_host_).count() : -1.0);
+  }
   const int D = spec_.d_model;
 
   // ---- host-side plan lowering ------------------------------------------------
@@ -858,7 +970,8 @@ void Impl::consume(const isim_batch_plan& p) {
   const std::int32_t* d_samples = reinterpret_cast<const std::int32_t*>(put(samples.data(), samples.size() * 4));
   const std::int32_t* d_frees0 = reinterpret_cast<const std::int32_t*>(put(frees0.data(), frees0.size() * 4));
   const std::int32_t* d_allocs0 = reinterpret_cast<const std::int32_t*>(put(allocs0.data(), allocs0.size() * 4));
-  IB2_CUDA(cudaMemcpyAsync(d, h, off, cudaMemcpyHostToDevice, main_));
+  launch_copy_from_host(d, plan_host_dev_[k], off, main_);
+  ++kernel_launches_;
   IB2_CUDA(cudaEventRecord(plan_done_[k], main_));
   h2d_bytes_ += static_cast<std::int64_t>(off);
 
@@ -883,10 +996,11 @@ void Impl::consume(const isim_batch_plan& p) {
     k1_bytes_iter_ = static_cast<double>(k1_bytes);
     max_pos1_ = 0;
     for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
+    if (!samples.empty() && !record_) sync_event(tok_done_[k], 1);  // tok_host_[k] free again
+    tok_out_host_ = record_ ? nullptr : tok_host_dev_[k];
     forward(n_rows, static_cast<int>(drows.size()), static_cast<int>(items.size()), static_cast<int>(samples.size()));
     if (!samples.empty() && !record_) {
-      sync_event(tok_done_[k], 1);
-      IB2_CUDA(cudaMemcpyAsync(tok_host_[k], out_tok_, samples.size() * 4, cudaMemcpyDeviceToHost, main_));
+      // The argmax kernel stored the ids into tok_host_[k] (mapped) directly.
       IB2_CUDA(cudaEventRecord(tok_done_[k], main_));
       d2h_bytes_ += static_cast<std::int64_t>(samples.size()) * 4;
     }
@@ -906,7 +1020,8 @@ void Impl::consume(const isim_batch_plan& p) {
     ring_ = (ring_ + 1) % kRing;
     sync_event(plan_done_[k2], 0);
     std::memcpy(plan_host_[k2], frees1.data(), frees1.size() * 4);
-    IB2_CUDA(cudaMemcpyAsync(plan_dev_[k2], plan_host_[k2], frees1.size() * 4, cudaMemcpyHostToDevice, main_));
+    launch_copy_from_host(plan_dev_[k2], plan_host_dev_[k2], frees1.size() * 4, main_);
+    ++kernel_launches_;
     h2d_bytes_ += static_cast<std::int64_t>(frees1.size()) * 4;
     IB2_CUDA(cudaEventRecord(plan_done_[k2], main_));
     launch_block_update(table_, stack_, top_, err_, reinterpret_cast<const std::int32_t*>(plan_dev_[k2]),
@@ -1022,7 +1137,8 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
   if (n_samples > 0) {
     launch_norm(x_, D, samples_dev_, n_samples, D, W(wl_.lnf_g), W(wl_.lnf_b), rms, m.norm_eps, lmrows_, D, main_);
     gemm(lmrows_, wl_.lm_w, m.vocab, D, Epi::StoreF32, wl_.lm_b, nullptr, 0, logits_, m.vocab, n_samples);
-    launch_argmax(logits_, n_samples, m.vocab, samples_dev_, rows_dev_, hist_, hist_stride_, out_tok_, main_);
+    launch_argmax(logits_, n_samples, m.vocab, samples_dev_, rows_dev_, hist_, hist_stride_, out_tok_, tok_out_host_,
+                  main_);
     kernel_launches_ += 2;
   }
 }
@@ -1050,6 +1166,13 @@ void Impl::sync() {
   }
   ev_pending_.clear();
   ev_bytes_.clear();
+  for (const SwapTrace& t : swap_trace_pending_) {
+    float a = 0.f, b = 0.f;
+    IB2_CUDA(cudaEventElapsedTime(&a, trace_ref_, t.t0));
+    IB2_CUDA(cudaEventElapsedTime(&b, trace_ref_, t.t1));
+    swap_trace_.push_back({static_cast<double>(t.iter), static_cast<double>(t.dir), a, b, t.bytes});
+  }
+  swap_trace_pending_.clear();
   for (std::size_t i = 0; i < swap_ev_pending_.size(); ++i) {
     float ms = 0.f;
     IB2_CUDA(cudaEventElapsedTime(&ms, swap_ev_pending_[i].first, swap_ev_pending_[i].second));
@@ -1066,9 +1189,23 @@ void Impl::sync() {
       IB2_CUDA(cudaEventElapsedTime(&fwd, iter_ev_[i][1], iter_ev_[i][2]));
       IB2_CUDA(cudaEventElapsedTime(&post, iter_ev_[i][2], iter_ev_[i + 1][0]));
       iter_ms_.push_back({pre, fwd, post});
+      const std::size_t gi = iter_ms_.size() - 1;  // global iteration index
+      double lead = -1e9;
+      if (trace_ref_ && gi < iter_host_ms_.size() && iter_host_ms_[gi] >= 0) {
+        float g = 0.f;
+        if (cudaEventElapsedTime(&g, trace_ref_, iter_ev_[i][0]) == cudaSuccess) lead = g - iter_host_ms_[gi];
+        else (void)cudaGetLastError();
+      }
+      iter_lead_ms_.push_back(lead);
       for (cudaEvent_t e : iter_ev_[i]) cudaEventDestroy(e);
     }
     iter_ev_.erase(iter_ev_.begin(), iter_ev_.end() - 1);
+  }
+  if (trace_iters_) {  // new reference point: GPU idle now
+    if (!trace_ref_) IB2_CUDA(cudaEventCreate(&trace_ref_));
+    IB2_CUDA(cudaEventRecord(trace_ref_, main_));
+    IB2_CUDA(cudaEventSynchronize(trace_ref_));
+    trace_ref_host_ = std::chrono::steady_clock::now();
   }
 }
 
@@ -1113,6 +1250,7 @@ std::string Impl::stats_json() const {
   j["samples"] = samples_total_;
   j["swap_in_tokens"] = swap_in_tok_;
   j["swap_out_tokens"] = swap_out_tok_;
+  j["swap_in_forwarded_tokens"] = swap_in_forwarded_tok_;
   j["swap_bytes"] = static_cast<double>(swap_in_tok_ + swap_out_tok_) * static_cast<double>(spec_.kv_bytes_per_token());
   j["gpu_blocks"] = gpu_blocks_;
   j["host_pool_bytes"] = host_bytes_;
@@ -1130,6 +1268,9 @@ std::string Impl::stats_json() const {
   j["host_consume_s"] = host_consume_s_;
   j["host_block_s"] = {host_block_s_[0], host_block_s_[1], host_block_s_[2], host_block_s_[3]};
   if (trace_iters_) {
+    j["iter_lead_ms"] = iter_lead_ms_;
+    j["iter_host_ms"] = iter_host_ms_;
+    j["swap_trace"] = swap_trace_;
     j["iter_ms"] = iter_ms_;
     j["iter_info"] = iter_info_;
   }

@@ -24,6 +24,7 @@
 
 #include "gemm_epilogue.cuh"
 #include "kernels.hpp"
+#include "tc_ptx.cuh"
 
 namespace ib2 {
 
@@ -33,35 +34,7 @@ namespace {
 
 constexpr int BM = 128, BK = 64, UMMA_K = 16;
 
-__device__ __forceinline__ std::uint32_t su32(const void* p) {
-  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(std::uint64_t* b, std::uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(std::uint64_t* b, std::uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          su32(dst)),
-      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(su32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
+using namespace tc;
 
 // Shared-memory matrix descriptor: K-major, 128-byte swizzle, 8-row atoms of
 // 1024 B (SBO), LBO unused, descriptor version 1 (sm_100).
@@ -331,17 +304,7 @@ __device__ __forceinline__ std::uint32_t map_to_rank(std::uint32_t local, std::u
 __device__ __forceinline__ void arrive_remote(std::uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
-__device__ __forceinline__ void wait_cluster(std::uint64_t* b, std::uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
+__device__ __forceinline__ void wait_cluster(std::uint64_t* b, std::uint32_t parity) { mbar_wait_cluster(b, parity); }
 
 template <int NT, int STAGES>
 __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant__ CUtensorMap map_w,

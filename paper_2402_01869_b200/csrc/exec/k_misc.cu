@@ -1,3 +1,4 @@
+#include <algorithm>
 // Bandwidth-bound helper kernels: weight init, K9 embedding, K5 norms,
 // K4 RoPE + paged KV write, K6 argmax, K8 block-table update, K7 swap copy.
 // All are HBM/latency bound; they use 16-byte vector accesses where the row
@@ -196,7 +197,8 @@ template <int NT>
 __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ logits, int V,
                                                    const std::int32_t* __restrict__ sample_rows,
                                                    const RowDesc* __restrict__ rows, std::int32_t* __restrict__ hist,
-                                                   int hist_stride, std::int32_t* __restrict__ out_tok) {
+                                                   int hist_stride, std::int32_t* __restrict__ out_tok,
+                                                   std::int32_t* __restrict__ out_host) {
   pdl_trigger();
   pdl_wait();
   const int s = blockIdx.x;
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(NT) argmax_kernel(const float* __restrict__ lo
     const RowDesc d = rows[sample_rows[s]];
     hist[static_cast<std::int64_t>(d.slot) * hist_stride + d.pos + 1] = idx;
     out_tok[s] = idx;
+    if (out_host) out_host[s] = idx;
   }
 }
 
@@ -300,7 +303,8 @@ __global__ void swap_copy_kernel(const SwapDesc* __restrict__ ops, const std::in
   const int D = H * hd;
   const int pb = table[static_cast<std::int64_t>(op.slot) * max_lb + pos / kBlockTokens];
   f16* blk = pool + layer * layer_stride + static_cast<std::int64_t>(pb) * block_stride;
-  f16* srow = stage + op.stage_off + (static_cast<std::int64_t>(layer) * op.n + i) * 2 * D;
+  const int ld = op.ld > 0 ? op.ld : op.n;
+  f16* srow = stage + op.stage_off + (static_cast<std::int64_t>(layer) * ld + i) * 2 * D;
   const int tok = pos % kBlockTokens;
   for (int v = threadIdx.x; v < 2 * D / 8; v += blockDim.x) {
     const int e = v * 8;
@@ -370,9 +374,30 @@ void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g,
 }
 
 void launch_argmax(const float* logits, int n, int V, const std::int32_t* sample_rows, const RowDesc* rows,
-                   std::int32_t* hist, int hist_stride, std::int32_t* out_tok, cudaStream_t s) {
+                   std::int32_t* hist, int hist_stride, std::int32_t* out_tok, std::int32_t* out_host, cudaStream_t s) {
   if (n <= 0) return;
-  launch_pdl(argmax_kernel<512>, dim3(n), dim3(512), 0, s, logits, V, sample_rows, rows, hist, hist_stride, out_tok);
+  launch_pdl(argmax_kernel<512>, dim3(n), dim3(512), 0, s, logits, V, sample_rows, rows, hist, hist_stride, out_tok,
+             out_host);
+  IB2_LAUNCH_CHECK();
+}
+
+// Small host -> device copies through the SMs from mapped pinned memory: the
+// copy engines may be busy for milliseconds with swap transfers, and a
+// cudaMemcpyAsync queued behind them would stall the compute stream.
+__global__ void copy_from_host_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, std::int64_t n16) {
+  pdl_trigger();
+  pdl_wait();
+  for (std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
+void launch_copy_from_host(void* dst, const void* src_mapped, std::size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  const std::int64_t n16 = static_cast<std::int64_t>((bytes + 15) / 16);
+  const int blocks = static_cast<int>(std::min<std::int64_t>((n16 + 255) / 256, 64));
+  launch_pdl(copy_from_host_kernel, dim3(blocks), dim3(256), 0, s, static_cast<uint4*>(dst),
+             static_cast<const uint4*>(src_mapped), n16);
   IB2_LAUNCH_CHECK();
 }
 

@@ -63,8 +63,13 @@ void launch_gemm(const GemmArgs& a, cudaStream_t s);
 bool gemm_uses_tcgen05();
 
 // K6: row argmax of fp32 logits, lowest index on ties; writes history.
+// out_host: mapped pinned memory the ids are also stored to (may be null).
 void launch_argmax(const float* logits, int n, int V, const std::int32_t* sample_rows, const RowDesc* rows,
-                   std::int32_t* hist, int hist_stride, std::int32_t* out_tok, cudaStream_t s);
+                   std::int32_t* hist, int hist_stride, std::int32_t* out_tok, std::int32_t* out_host, cudaStream_t s);
+
+// Small H2D copy performed by SMs from mapped pinned memory (bytes rounded up
+// to 16; both buffers must have that slack).
+void launch_copy_from_host(void* dst, const void* src_mapped, std::size_t bytes, cudaStream_t s);
 
 void launch_gather_rows(const f16* src, int ld, const std::int32_t* rows, int n, int D, f16* dst,
                         cudaStream_t s);

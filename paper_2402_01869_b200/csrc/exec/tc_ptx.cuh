@@ -6,6 +6,7 @@
 #include <cuda.h>
 
 #include <cstdint>
+#include <cstdio>
 
 namespace ib2 {
 namespace tc {
@@ -23,16 +24,55 @@ __device__ __forceinline__ void mbar_expect_tx(std::uint64_t* b, std::uint32_t b
 __device__ __forceinline__ void mbar_arrive(std::uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
+// Bounded waits: a phase that does not complete within ~2^34 cycles (about
+// 9 s) means a protocol bug; the kernel prints the barrier and traps (the
+// launch fails loudly) instead of wedging the GPU.
+__device__ __forceinline__ bool mbar_try(std::uint32_t addr, std::uint32_t parity) {
+  std::uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(su32(b)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_cluster(std::uint32_t addr, std::uint32_t parity) {
+  std::uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __noinline__ inline void mbar_timeout(std::uint32_t addr, std::uint32_t parity) {
+  printf("ib2 watchdog: mbarrier smem+0x%x parity %u stuck, block (%d,%d,%d) thread %d\n", addr, parity, blockIdx.x,
+         blockIdx.y, blockIdx.z, threadIdx.x);
+  __trap();
+}
+constexpr long long kWaitLimitCycles = 1LL << 34;
+__device__ __forceinline__ void mbar_wait(std::uint64_t* b, std::uint32_t parity) {
+  const std::uint32_t a = su32(b);
+  if (mbar_try(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(a, parity))
+    if (clock64() - t0 > kWaitLimitCycles) mbar_timeout(a, parity);
+}
+// Acquire at cluster scope (barriers signalled from peer CTAs over DSMEM).
+__device__ __forceinline__ void mbar_wait_cluster(std::uint64_t* b, std::uint32_t parity) {
+  const std::uint32_t a = su32(b);
+  if (mbar_try_cluster(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_cluster(a, parity))
+    if (clock64() - t0 > kWaitLimitCycles) mbar_timeout(a, parity);
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, std::uint64_t* bar, int c0, int c1) {

@@ -45,3 +45,8 @@ show("swap-in only", (sin > 0) & (sout == 0))
 show("swap-out only", (sout > 0) & (sin == 0))
 show("both directions", (sin > 0) & (sout > 0))
 show("all", ms > -1)
+if len(sys.argv) > 3:
+    import json
+    json.dump({"phases": ph.tolist(), "info": info.tolist(), "lead": st["iter_lead_ms"][k0:k0 + len(ph)],
+               "host": st["iter_host_ms"][k0:k0 + len(ph)], "swaps": st["swap_trace"], "k0": k0},
+              open(sys.argv[3], "w"))
