@@ -44,6 +44,15 @@ WORKLOAD_NAME = ("C1: GPT-J-6B-shaped random-init fp16 model, Math/QA/Chatbot AP
                  "InferCept min-waste policy, reference cost-model defaults, 150 GB KV pool")
 
 
+def k1_traffic():
+    """ncu-measured DRAM bytes of one K1 launch vs its algorithmic bytes
+    (profiles/k1_traffic.json, written by tools/ncu_traffic.py)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "k1_traffic.json")))
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -134,6 +143,27 @@ def cpu_forward_sample(plans, n_plans=3):
     return per_iter, dict(t1=t1, t2=t2)
 
 
+def measure_link(torch, mb=512, reps=3):
+    """Pinned host <-> device copy bandwidth on this box (the swap roofline)."""
+    n = mb << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        with torch.cuda.stream(s):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                fn()
+            e1.record(s)
+        torch.cuda.synchronize()
+        out[name] = reps * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del h, d
+    return out
+
+
 def run_b200(args):
     import torch
     import paper_2402_01869_b200 as ib
@@ -146,6 +176,7 @@ def run_b200(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    link = measure_link(torch)
     tmp = tempfile.mkdtemp()
     trace = shard_trace(ib, world, rank, tmp)
     cost = ib.CostModel.from_json(COST)
@@ -227,10 +258,19 @@ def run_b200(args):
         "swap_gbs_achieved": swap_gbs,
         "swap_tokens_in_window": tot["swapped"],
         "swap_in_forwarded_tokens": tot["fwd_tok"],
+        "swap_roofline": {"bound": "host link", "achieved": swap_gbs, "unit": "GB/s",
+                          "peak": (link["h2d"] + link["d2h"]) / 2, "peak_h2d": link["h2d"], "peak_d2h": link["d2h"],
+                          "frac": swap_gbs / ((link["h2d"] + link["d2h"]) / 2) if swap_gbs else None,
+                          "peak_source": "pinned 512 MiB copies measured by bench.py on this box",
+                          "note": "achieved = swapped bytes / time of each PCIe batch on the copy streams; "
+                                  "swap-ins forwarded from swap-out staging do not cross the link"},
         "roofline": {"bound": "hbm", "kernel": "K1 paged decode attention (middle layer, every timed iteration)",
                      "achieved": k1_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": (k1_gbs / pk["hbm_gbs"]) if k1_gbs and pk.get("hbm_gbs") else None,
-                     "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                     "traffic": (k1_traffic() or {}).get("dram_bytes_per_launch"),
+                     "traffic_algorithmic_bytes": (k1_traffic() or {}).get("algorithmic_bytes_per_launch"),
+                     "traffic_source": (k1_traffic() or {}).get("source"),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "e2e": {"value": tot["completed"] / wall_s, "unit": "req/s",
                 "h2d_bytes_per_step": tot["h2d"] / args.steps / world,
                 "d2h_bytes_per_step": tot["d2h"] / args.steps / world},
