@@ -116,7 +116,22 @@ enum class Epi : int {
   GeluF16 = 1,      // out = gelu_tanh(acc + bias)
   ResidAdd = 2,      // resid(fp32) += acc (+bias)
   SwiGluF16 = 3,    // out[j] = silu(acc[2j]) * acc[2j+1]
-  StoreF32 = 4       // outf = acc (+bias)
+  StoreF32 = 4,      // outf = acc (+bias)
+  QkvRopeKv = 5      // fused K4: q -> out (RoPE), k (RoPE), v -> paged KV pool
+};
+
+// Epi::QkvRopeKv: the QKV projection's epilogue applies the interleaved
+// (GPT-J) rotary embedding to q and k after the same f16 rounding as a
+// separate pass would, stores q to `out`, and writes k and v of each row
+// straight into its paged KV block.
+struct QkvWrite {
+  const RowDesc* rows;  // [M] slot, position of each row
+  f16* pool;            // [L][blocks][2][H][16][hd]
+  std::int64_t layer_off, block_stride;
+  const std::int32_t* table;
+  int max_lb;
+  int H, hd, rot;        // rot: rotary dims (interleaved pairs), 0 = none
+  const float* rope_cs;  // [pos][rot/2][cos, sin]
 };
 
 struct GemmArgs {
@@ -129,6 +144,7 @@ struct GemmArgs {
   int ldo;
   float* outf;         // fp32 output / residual stream
   int ldf;
+  QkvWrite qkv;        // Epi::QkvRopeKv only
 };
 
 }  // namespace ib2

@@ -1085,15 +1085,31 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
     launch_gemm(ga, main_);
     ++kernel_launches_;
   };
+  // Interleaved (GPT-J) or no rotary: RoPE pairs are adjacent columns, so the
+  // QKV GEMM epilogue can apply it and write K/V into the pool itself.
+  // Opt-in (IB2_FUSED_QKV=1): measured 2.5 % slower end to end than the
+  // separate K4 pass on C1 -- the epilogue's dependent row/table loads sit on
+  // the QKV GEMM's critical path (one tile per CTA), costing more than K4.
+  static const bool want_fuse = getenv("IB2_FUSED_QKV") != nullptr;
+  const bool fused_qkv = want_fuse && (m.rotary_dim == 0 || m.family == Family::GptJ) && D % 64 == 0;
   launch_embed(rows_dev_, n, hist_, hist_stride_, W(wl_.tok_emb), W(wl_.pos_emb), D, m.token_seed, m.vocab, x_, main_);
   ++kernel_launches_;
   const int timed_layer = m.layers / 2;
   for (int l = 0; l < m.layers; ++l) {
     const LayerWeights& lw = wl_.layer[l];
     launch_norm(x_, D, nullptr, n, D, W(lw.ln1_g), W(lw.ln1_b), rms, m.norm_eps, xn_, D, main_);
-    gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreF16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
-    launch_rope_kv_write(qkv_, rows_dev_, n, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, main_);
-    kernel_launches_ += 2;
+    if (fused_qkv) {
+      // K4 fused into the QKV epilogue: q (RoPE) -> qkv_, k (RoPE) / v -> pool.
+      GemmArgs ga{xn_, weights_ + lw.w_qkv, n, 3 * D, D, Epi::QkvRopeKv, W(lw.b_qkv), qkv_, 3 * D, nullptr, 0,
+                  QkvWrite{rows_dev_, g.pool, l * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks,
+                           m.heads, m.head_dim(), m.rotary_dim, rope_cs_}};
+      launch_gemm(ga, main_);
+      ++kernel_launches_;
+    } else {
+      gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreF16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
+      launch_rope_kv_write(qkv_, rows_dev_, n, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, main_);
+      kernel_launches_ += 2;
+    }
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     const bool time_k1 = timing_ && l == timed_layer && n_drows > 0;
     if (time_k1) {

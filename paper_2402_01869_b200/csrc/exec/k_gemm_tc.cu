@@ -243,6 +243,49 @@ __device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v
 // load is issued before any store so the 16 residual read-modify-writes
 // overlap instead of paying one memory latency each.
 __device__ __forceinline__ void epi_rows16(const GemmArgs& a, int n, int m0, const float* v, int lane) {
+  if (a.epi == Epi::QkvRopeKv) {
+    // Thread = column n (fixed part / head / dim), 16 tokens.  Rotary pairs
+    // are columns (2i, 2i+1): neighbouring lanes.
+    const QkvWrite& w = a.qkv;
+    const int D = w.H * w.hd;
+    const int part = n >= D ? (n >= 2 * D ? 2 : 1) : 0;
+    const int hn = n - part * D, h = hn / w.hd, d = hn - h * w.hd;
+    const bool rot = part < 2 && d < w.rot;
+    const float b = (a.bias && n < a.N) ? __half2float(a.bias[n]) : 0.f;
+    float x[16], pr[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) x[j] = __half2float(__float2half_rn(v[j] + b));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) pr[j] = __shfl_xor_sync(0xffffffffu, x[j], 1);
+    if (n >= a.N) return;
+    int pos[16];
+    std::int32_t pb[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) pos[j] = m0 + j < a.M ? w.rows[m0 + j].pos : 0;
+    if (part > 0) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        pb[j] = m0 + j < a.M ? w.table[static_cast<std::int64_t>(w.rows[m0 + j].slot) * w.max_lb + pos[j] / kBlockTokens]
+                             : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (m0 + j >= a.M) break;
+      float y = x[j];
+      if (rot) {
+        const float2 cs = *reinterpret_cast<const float2*>(w.rope_cs + (static_cast<std::int64_t>(pos[j]) * (w.rot / 2) + d / 2) * 2);
+        y = (d & 1) ? __fadd_rn(__fmul_rn(x[j], cs.x), __fmul_rn(pr[j], cs.y))
+                    : __fsub_rn(__fmul_rn(x[j], cs.x), __fmul_rn(pr[j], cs.y));
+      }
+      const f16 hv = __float2half_rn(y);
+      if (part == 0)
+        a.out[static_cast<std::int64_t>(m0 + j) * a.ldo + n] = hv;
+      else
+        w.pool[w.layer_off + static_cast<std::int64_t>(pb[j]) * w.block_stride +
+               ((static_cast<std::int64_t>(part - 1) * w.H + h) * kBlockTokens + pos[j] % kBlockTokens) * w.hd + d] = hv;
+    }
+    return;
+  }
   if (a.epi == Epi::SwiGluF16) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
@@ -531,6 +574,14 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
 // 16 consecutive output columns n0.. of row m (vector stores when aligned).
 __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, float* v) {
   if (m >= a.M || n0 >= a.N) return;
+  if (a.epi == Epi::QkvRopeKv) {  // 16 columns of one head part; rotary pairs inside
+    float x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      x[i] = __half2float(__float2half_rn(v[i] + (a.bias ? __half2float(a.bias[n0 + i]) : 0.f)));
+    if (n0 + 16 <= a.N) qkv_store16(a, m, n0, x);
+    return;
+  }
   const bool full = n0 + 16 <= a.N;
   if (a.bias && a.epi != Epi::SwiGluF16) {
 #pragma unroll
