@@ -154,6 +154,7 @@ class Impl final : public B200Executor {
   std::size_t host_alloc(std::size_t bytes);
   bool record_ = false, timing_ = false;
   bool force_row_attention_ = false;  // diagnostics: every row through K1
+  bool fused_qkv_ = false;            // K4 in the QKV GEMM epilogue (opt-in)
   // diagnostics: per-iteration start events on the compute stream + the
   // iteration's composition (rows, decode rows, chunk rows, swap-in, swap-out)
   bool trace_iters_ = false;
@@ -339,6 +340,7 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   record_ = pj.value("record", false);
   timing_ = pj.value("timing", false);
   force_row_attention_ = pj.value("row_attention", false);
+  fused_qkv_ = pj.value("fused_qkv", getenv("IB2_FUSED_QKV") != nullptr);
   trace_iters_ = pj.value("trace_iterations", false);
 
   max_slots_ = pj.value("max_requests", 1024);
@@ -1090,8 +1092,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
   // Opt-in (IB2_FUSED_QKV=1): measured 2.5 % slower end to end than the
   // separate K4 pass on C1 -- the epilogue's dependent row/table loads sit on
   // the QKV GEMM's critical path (one tile per CTA), costing more than K4.
-  static const bool want_fuse = getenv("IB2_FUSED_QKV") != nullptr;
-  const bool fused_qkv = want_fuse && (m.rotary_dim == 0 || m.family == Family::GptJ) && D % 64 == 0;
+  const bool fused_qkv = fused_qkv_ && (m.rotary_dim == 0 || m.family == Family::GptJ) && D % 64 == 0;
   launch_embed(rows_dev_, n, hist_, hist_stride_, W(wl_.tok_emb), W(wl_.pos_emb), D, m.token_seed, m.vocab, x_, main_);
   ++kernel_launches_;
   const int timed_layer = m.layers / 2;
