@@ -29,6 +29,16 @@ constexpr int kBlockTokens = 16;  // paged KV block = 16 token positions
 // its predecessor's completion before touching global memory it produced.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Loads through `const __restrict__` pointers become ld.global.nc, which the
+// compiler treats as invariant and may hoist above griddepcontrol.wait (it
+// did, in K1: the row descriptors of the previous iteration were read).
+// Passing a pointer through an asm volatile after pdl_wait() makes every load
+// through it depend on the wait.  tests/test_sass.py checks the .so.
+template <typename T>
+__device__ __forceinline__ T* after_wait(T* p) {
+  asm volatile("" : "+l"(p));
+  return p;
+}
 
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s,

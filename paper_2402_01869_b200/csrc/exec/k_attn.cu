@@ -155,13 +155,13 @@ __global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
 }
 
 __global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows, int H,
-                                      int HD, int max_splits, const float* __restrict__ part_o,
+                                      int HD, int max_splits, int split_len, const float* __restrict__ part_o,
                                       const float* __restrict__ part_ml, f16* __restrict__ out) {
   pdl_trigger();
   pdl_wait();
   const int dr = blockIdx.x, h = blockIdx.y;
   const int r = drow[dr];
-  const int ns = (rows[r].pos + 1 + kSplit - 1) / kSplit;
+  const int ns = (rows[r].pos + 1 + split_len - 1) / split_len;
   const std::int64_t base = (static_cast<std::int64_t>(dr) * H + h) * max_splits;
   float M = -FLT_MAX;
   for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
@@ -177,13 +177,14 @@ __global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, con
 
 template <int HD>
 void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
-                      int layer, int max_splits, float* part_o, float* part_ml, f16* out, cudaStream_t s) {
+                      int layer, int max_pos1, float* part_o, float* part_ml, f16* out, cudaStream_t s) {
+  const int max_splits = (max_pos1 + kSplit - 1) / kSplit;
   dim3 grid(max_splits, g.heads, n);
   launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
              layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml);
   IB2_LAUNCH_CHECK();
-  launch_pdl(decode_combine_kernel, dim3(n, g.heads), dim3(HD), 0, s, drow, rows, g.heads, HD, max_splits, part_o,
-             part_ml, out);
+  launch_pdl(decode_combine_kernel, dim3(n, g.heads), dim3(HD), 0, s, drow, rows, g.heads, HD, max_splits, kSplit,
+             part_o, part_ml, out);
   IB2_LAUNCH_CHECK();
 }
 
@@ -193,11 +194,10 @@ void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const Row
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
                              f16* out, cudaStream_t s) {
   if (n_drows <= 0) return;
-  const int max_splits = (max_pos_plus1 + kSplit - 1) / kSplit;
   switch (g.head_dim) {
-    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_splits, part_o, part_ml, out, s); break;
-    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_splits, part_o, part_ml, out, s); break;
-    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_splits, part_o, part_ml, out, s); break;
+    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
+    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
+    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
     default: throw DeviceError("unsupported head_dim");
   }
 }

@@ -685,6 +685,11 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
+  // Both CTAs of the pair must be running before the 2-CTA TMEM allocation:
+  // its hand-shake signals the peer through shared memory, and a signal sent
+  // before the peer CTA started is lost (observed: the peer's allocator warp
+  // waiting forever while the leader sat in the cluster barrier below).
+  asm volatile("barrier.cluster.arrive.aligned;\nbarrier.cluster.wait.aligned;\n" ::: "memory");
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
                  "r"(512));
