@@ -98,8 +98,18 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def workload_for(world):
+    """The trace the N replicas serve: 2000*N requests at 3*N/s (same class mix
+    and seed), so each replica's id-mod-N shard is statistically the C1 trace:
+    per-GPU work is fixed as N grows (weak scaling)."""
+    if world == 1:
+        return WORKLOAD
+    return dict(WORKLOAD, request_count=WORKLOAD["request_count"] * world,
+                arrival_rate=WORKLOAD["arrival_rate"] * world)
+
+
 def shard_trace(ib, world, rank, tmpdir):
-    trace = ib.Trace.generate(WORKLOAD)
+    trace = ib.Trace.generate(workload_for(world))
     if world == 1:
         return trace
     full = os.path.join(tmpdir, "full.jsonl")
@@ -251,13 +261,17 @@ def run_b200(args):
         "data": "synthetic (generated API trace, random-init weights, synthetic token ids)",
         "config": {"workload": WORKLOAD_NAME, "window_iterations": [args.fast_forward + args.warmup + 1,
                                                                     args.fast_forward + args.warmup + args.steps],
-                   "fast_forward_untimed": args.fast_forward, "parallelism": f"replicas{world} (request id mod N)",
+                   "fast_forward_untimed": args.fast_forward,
+                   "parallelism": f"replicas{world}: one engine + KV pool per GPU serving request ids = rank mod N of a "
+                                  f"{workload_for(world)['request_count']}-request trace at "
+                                  f"{workload_for(world)['arrival_rate']:g}/s (per-GPU load = C1)",
                    "l2": "inputs larger than L2 (KV pool ~154 GB; ~15 GB of KV read per iteration)"},
         "decode_tok_s": tot["decode"] / dev_s,
         "completed_in_window": tot["completed"],
         "swap_gbs_achieved": swap_gbs,
         "swap_tokens_in_window": tot["swapped"],
         "swap_in_forwarded_tokens": tot["fwd_tok"],
+        "host_pool_peak_gb": s1["host_pool_peak"] / 1e9,
         "swap_roofline": {"bound": "host link", "achieved": swap_gbs, "unit": "GB/s",
                           "peak": (link["h2d"] + link["d2h"]) / 2, "peak_h2d": link["h2d"], "peak_d2h": link["d2h"],
                           "frac": swap_gbs / ((link["h2d"] + link["d2h"]) / 2) if swap_gbs else None,

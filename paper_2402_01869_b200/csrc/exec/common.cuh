@@ -155,6 +155,7 @@ struct GemmArgs {
   float* outf;         // fp32 output / residual stream
   int ldf;
   QkvWrite qkv;        // Epi::QkvRopeKv only
+  int no_early_w;      // diagnostics: no weight prefetch before griddepcontrol.wait
 };
 
 }  // namespace ib2

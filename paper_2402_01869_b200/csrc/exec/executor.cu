@@ -53,6 +53,7 @@ class HostArena {
         free_.erase(it);
         if (left) free_[off + n] = left;
         used_ += n;
+        peak_ = std::max(peak_, used_);
         return off;
       }
     }
@@ -77,10 +78,11 @@ class HostArena {
     }
   }
   std::size_t used() const { return used_; }
+  std::size_t peak() const { return peak_; }
 
  private:
   std::map<std::size_t, std::size_t> free_;
-  std::size_t cap_ = 0, used_ = 0;
+  std::size_t cap_ = 0, used_ = 0, peak_ = 0;
 };
 
 // Positions [lo,hi) of one request living in a host extent laid out
@@ -1272,6 +1274,7 @@ std::string Impl::stats_json() const {
   j["gpu_blocks"] = gpu_blocks_;
   j["host_pool_bytes"] = host_bytes_;
   j["host_pool_used"] = arena_.used();
+  j["host_pool_peak"] = arena_.peak();
   j["kernel_launches"] = kernel_launches_;
   j["k1_timed_launches"] = k1_launches_timed_;
   j["k1_ms"] = k1_ms_;

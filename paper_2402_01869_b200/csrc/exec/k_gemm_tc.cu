@@ -401,20 +401,31 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
   pdl_trigger();
-  pdl_wait();  // the prologue above overlapped the predecessor kernel
 
   if (warp == 0) {
     if (lane == 0) {
-      int i = 0;
-      for (int t = t0; t < t1; ++t)
-        for (int kb = kb0; kb < kb1; ++kb, ++i) {
-          const int st = i % STAGES;
-          if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
-          unsigned char* sw = smem + st * L::STAGE_BYTES;
-          mbar_expect_tx(&full[st], L::STAGE_BYTES);
-          tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
-          tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
-        }
+      // Weights do not depend on the predecessor kernel: the first ring's
+      // worth of weight tiles streams in while it is still finishing; the
+      // activation tiles follow griddepcontrol.wait.
+      const int per_tile = kb1 - kb0, total = (t1 - t0) * per_tile;
+      const int early = args.no_early_w ? 0 : (total < STAGES ? total : STAGES);
+      for (int i = 0; i < early; ++i) {
+        const int t = t0 + i / per_tile, kb = kb0 + i % per_tile;
+        mbar_expect_tx(&full[i], L::STAGE_BYTES);
+        tma_load_2d(smem + i * L::STAGE_BYTES, &map_w, &full[i], 0, (t * kblocks + kb) * BM);
+      }
+      pdl_wait();
+      for (int i = 0; i < early; ++i)
+        tma_load_2d(smem + i * L::STAGE_BYTES + L::A_BYTES, &map_a, &full[i], (kb0 + i % per_tile) * BK, 0);
+      for (int i = early; i < total; ++i) {
+        const int t = t0 + i / per_tile, kb = kb0 + i % per_tile;
+        const int st = i % STAGES;
+        mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
+        unsigned char* sw = smem + st * L::STAGE_BYTES;
+        mbar_expect_tx(&full[st], L::STAGE_BYTES);
+        tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
+        tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -453,6 +464,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // the epilogue reads / writes buffers of earlier kernels
     const int q = warp - 4, row = q * 32 + lane;
     const int mcols = min(args.M, NT);
     const int m_lo = rank * mcols / S, m_hi = (rank + 1) * mcols / S;
@@ -701,11 +713,21 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
   pdl_trigger();
-  pdl_wait();  // the prologue above overlapped the predecessor kernel
 
   if (warp == 0) {
     if (lane == 0) {
       const std::uint32_t full0 = mapa_rank(su32(full), 0);  // leader's full barriers
+      // The weight tiles of the first ring's worth of k blocks stream in
+      // before griddepcontrol.wait (they do not depend on the predecessor).
+      int pre = 0;
+      for (int t = pair; t < total && pre < STAGES && !args.no_early_w; t += npairs) {
+        const int wtile = (t / MT) * 2 + static_cast<int>(rank);
+        for (int kb = 0; kb < nk && pre < STAGES; ++kb, ++pre) {
+          if (leader) mbar_expect_tx(&full[pre], 2 * L::STAGE_BYTES);
+          tma_load_2d_pair(smem + pre * L::STAGE_BYTES + L::A_BYTES, &map_w, full0 + pre * 8, 0, (wtile * nk + kb) * 128);
+        }
+      }
+      pdl_wait();
       int i = 0;
       for (int t = pair; t < total; t += npairs) {
         const int mt = t % MT, ntl = t / MT;
@@ -713,10 +735,14 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
         const int wtile = ntl * 2 + static_cast<int>(rank);  // this CTA's 128-row weight tile
         for (int kb = 0; kb < nk; ++kb, ++i) {
           const int st = i % STAGES;
-          if (i >= STAGES) mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
-          if (leader) mbar_expect_tx(&full[st], 2 * L::STAGE_BYTES);
           unsigned char* sa = smem + st * L::STAGE_BYTES;
           const std::uint32_t bar = full0 + st * 8;
+          if (i < pre) {  // weights already in flight
+            tma_load_2d_pair(sa, &map_a, bar, kb * BK, arow);
+            continue;
+          }
+          mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
+          if (leader) mbar_expect_tx(&full[st], 2 * L::STAGE_BYTES);
           tma_load_2d_pair(sa, &map_a, bar, kb * BK, arow);
           tma_load_2d_pair(sa + L::A_BYTES, &map_w, bar, 0, (wtile * nk + kb) * 128);
         }
@@ -763,6 +789,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       }
     }
   } else if (warp >= 4) {
+    pdl_wait();  // the epilogue reads / writes buffers of earlier kernels
     const int q = warp - 4;
     const std::uint32_t tempty0 = mapa_rank(su32(tempty), 0);
     int seg = 0;
@@ -1026,8 +1053,11 @@ CUtensorMap make_tmap_2d(const void* base, std::int64_t inner, std::int64_t rows
 
 bool gemm_uses_tcgen05() { return true; }
 
-void launch_gemm(const GemmArgs& a, cudaStream_t s) {
-  if (a.M <= 0) return;
+void launch_gemm(const GemmArgs& a_in, cudaStream_t s) {
+  if (a_in.M <= 0) return;
+  static const bool no_early = getenv("IB2_NO_EARLY_W") != nullptr;  // diagnostics
+  GemmArgs a = a_in;
+  a.no_early_w = no_early ? 1 : 0;
   if (a.K % BK != 0 || a.N % 2 != 0) {  // N tails are masked; K must fill whole 64-wide blocks
     launch_gemm_simt(a, s);
     return;

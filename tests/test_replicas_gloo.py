@@ -60,9 +60,13 @@ def test_two_rank_request_sharding():
     mp.spawn(_worker, args=(2, _free_port(), outdir), nprocs=2, join=True)
     got = json.load(open(os.path.join(outdir, "gathered.json")))
     ids0, ids1 = set(got[0]["ids"]), set(got[1]["ids"])
-    assert ids0.isdisjoint(ids1) and ids0 | ids1 == set(range(WL["request_count"]))
+    # bench.workload_for: the 2-replica trace has 2x the requests at 2x the rate,
+    # so each shard carries the single-GPU load (weak scaling).
+    n = 2 * WL["request_count"]
+    assert ids0.isdisjoint(ids1) and ids0 | ids1 == set(range(n))
     assert all(i % 2 == 0 for i in ids0) and all(i % 2 == 1 for i in ids1)
-    assert sum(g["completed"] for g in got) == WL["request_count"]
+    assert sum(g["completed"] for g in got) == n
+    assert abs(len(ids0) - WL["request_count"]) <= 1
     # Each rank's schedule equals running its shard alone in this process.
     import paper_2402_01869_b200 as ib
     for g in got:
