@@ -156,6 +156,7 @@ struct GemmArgs {
   int ldf;
   QkvWrite qkv;        // Epi::QkvRopeKv only
   int no_early_w;      // diagnostics: no weight prefetch before griddepcontrol.wait
+  const float* addf;   // Epi::ResidAdd: if set, outf = (outf + acc) + addf (same [M][ldf] layout)
 };
 
 }  // namespace ib2

@@ -101,7 +101,10 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& a, int m, int n0,
       float* o = a.outf + static_cast<std::int64_t>(m) * a.ldf + n0;
 #pragma unroll
       for (int i = 0; i < CNT; ++i)
-        if (n0 + i < a.N) o[i] += v[i];
+        if (n0 + i < a.N) {
+          const float r = o[i] + v[i];
+          o[i] = a.addf ? r + a.addf[static_cast<std::int64_t>(m) * a.ldf + n0 + i] : r;
+        }
       break;
     }
     case Epi::StoreF32: {

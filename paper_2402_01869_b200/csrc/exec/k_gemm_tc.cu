@@ -221,7 +221,12 @@ __device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v
   switch (a.epi) {
     case Epi::StoreF16: a.out[static_cast<std::int64_t>(m) * a.ldo + n] = __float2half_rn(v); break;
     case Epi::GeluF16: a.out[static_cast<std::int64_t>(m) * a.ldo + n] = __float2half_rn(gelu_tanh(v)); break;
-    case Epi::ResidAdd: a.outf[static_cast<std::int64_t>(m) * a.ldf + n] += v; break;
+    case Epi::ResidAdd: {
+      const std::int64_t i = static_cast<std::int64_t>(m) * a.ldf + n;
+      const float r = a.outf[i] + v;
+      a.outf[i] = a.addf ? r + a.addf[i] : r;
+      break;
+    }
     case Epi::StoreF32: a.outf[static_cast<std::int64_t>(m) * a.ldf + n] = v; break;
     default: break;
   }
@@ -311,9 +316,16 @@ __device__ __forceinline__ void epi_rows16(const GemmArgs& a, int n, int m0, con
       float old[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) old[j] = m0 + j < a.M ? a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] : 0.f;
+      float add[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (m0 + j < a.M) a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] = old[j] + (v[j] + b);
+        add[j] = (a.addf && m0 + j < a.M) ? a.addf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < a.M) {
+          const float r = old[j] + (v[j] + b);
+          a.outf[static_cast<std::int64_t>(m0 + j) * a.ldf + n] = a.addf ? r + add[j] : r;
+        }
       break;
     }
     case Epi::StoreF32:
@@ -629,18 +641,35 @@ __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, flo
       if (full && (a.ldf % 4) == 0) {
         float4* o4 = reinterpret_cast<float4*>(o);
         if (a.epi == Epi::ResidAdd) {
-          float4 r[4];
+          float4 r[4], ad[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) r[i] = o4[i];
+          if (a.addf) {
+            const float4* a4 = reinterpret_cast<const float4*>(a.addf + static_cast<std::int64_t>(m) * a.ldf + n0);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            o4[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1], r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+            for (int i = 0; i < 4; ++i) ad[i] = a4[i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o4[i] = make_float4((r[i].x + v[4 * i]) + ad[i].x, (r[i].y + v[4 * i + 1]) + ad[i].y,
+                                  (r[i].z + v[4 * i + 2]) + ad[i].z, (r[i].w + v[4 * i + 3]) + ad[i].w);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              o4[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1], r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+          }
         } else {
 #pragma unroll
           for (int i = 0; i < 4; ++i) o4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         }
       } else {
-        for (int i = 0; i < 16 && n0 + i < a.N; ++i) o[i] = a.epi == Epi::ResidAdd ? o[i] + v[i] : v[i];
+        for (int i = 0; i < 16 && n0 + i < a.N; ++i) {
+          if (a.epi != Epi::ResidAdd) {
+            o[i] = v[i];
+            continue;
+          }
+          const float r = o[i] + v[i];
+          o[i] = a.addf ? r + a.addf[static_cast<std::int64_t>(m) * a.ldf + n0 + i] : r;
+        }
       }
       break;
     }

@@ -118,15 +118,16 @@ def _small_family_plans(tmp_path, n=24):
 
 
 @pytest.mark.skipif(not have_gpu(), reason="needs a B200")
-@pytest.mark.parametrize("fused_qkv", [False, True])
-def test_gptj_family_small_parity(tmp_path, fused_qkv):
+@pytest.mark.parametrize("fused_qkv,overlap_mlp", [(False, True), (True, True), (False, False)])
+def test_gptj_family_small_parity(tmp_path, fused_qkv, overlap_mlp):
     # GPT-J block structure at reduced width: head_dim 256, interleaved rotary
     # 64, parallel residual, LM-head bias; optionally RoPE + KV write fused
-    # into the QKV GEMM epilogue.
+    # into the QKV GEMM epilogue; the MLP branch on the second stream or inline.
     plans, cost = _small_family_plans(tmp_path)
     model = {"preset": "gptj-6b", "layers": 2, "d_model": 1024, "heads": 4, "ffn": 4096, "vocab": 8192,
              "max_pos": 1088}
-    r = replay(plans, model, pools_for(cost, 2 * 2 * 1024 * 2, max_ctx=1088, fused_qkv=fused_qkv), 250,
+    r = replay(plans, model, pools_for(cost, 2 * 2 * 1024 * 2, max_ctx=1088, fused_qkv=fused_qkv,
+                                                overlap_mlp=overlap_mlp), 250,
                check_tables_every=10)
     assert r["sampled"] > 100
     print("gptj-small parity", {k: v for k, v in r.items() if k != "stats"})
