@@ -1386,12 +1386,15 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
   const KvGeom g = geom();
   const std::size_t row = static_cast<std::size_t>(2 * D) * 2;
   const auto ex = extents_.find(rid);
-  for (std::int64_t p = lo; p < hi; ++p) {
-    const Extent* on_host = nullptr;
-    if (ex != extents_.end())
-      for (const Extent& x : ex->second)
-        if (x.lo <= p && p < x.hi) on_host = &x;
-    for (std::int64_t l = 0; l < L; ++l) {
+  // One D2H per (layer, block) of the GPU-resident positions.
+  std::vector<f16> blk(static_cast<std::size_t>(2 * H * kBlockTokens * hd));
+  std::int64_t cached_l = -1, cached_pb = -1;
+  for (std::int64_t l = 0; l < L; ++l) {
+    for (std::int64_t p = lo; p < hi; ++p) {
+      const Extent* on_host = nullptr;
+      if (ex != extents_.end())
+        for (const Extent& x : ex->second)
+          if (x.lo <= p && p < x.hi) on_host = &x;
       f16* d = dst + (l * n + (p - lo)) * 2 * D;
       if (on_host) {
         const std::int64_t n0 = on_host->hi0 - on_host->lo0;
@@ -1400,12 +1403,15 @@ void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out
       }
       const std::int32_t pb = t[p / kBlockTokens];
       if (pb < 0) throw DeviceError("read_kv: position neither on the GPU nor on the host");
+      if (l != cached_l || pb != cached_pb) {
+        IB2_CUDA(cudaMemcpy(blk.data(), pool_ + l * g.layer_stride() + static_cast<std::int64_t>(pb) * g.block_stride(),
+                            blk.size() * sizeof(f16), cudaMemcpyDeviceToHost));
+        cached_l = l;
+        cached_pb = pb;
+      }
       for (int kv = 0; kv < 2; ++kv)
-        for (std::int64_t h = 0; h < H; ++h) {
-          const f16* src = pool_ + l * g.layer_stride() + static_cast<std::int64_t>(pb) * g.block_stride() +
-                            ((kv * H + h) * kBlockTokens + p % kBlockTokens) * hd;
-          IB2_CUDA(cudaMemcpy(d + kv * D + h * hd, src, hd * 2, cudaMemcpyDeviceToHost));
-        }
+        for (std::int64_t h = 0; h < H; ++h)
+          std::memcpy(d + kv * D + h * hd, blk.data() + ((kv * H + h) * kBlockTokens + p % kBlockTokens) * hd, hd * 2);
     }
   }
 }
