@@ -934,7 +934,7 @@ void Impl::consume(const isim_batch_plan& p) {
     throw DeviceError("executor: more sampling / decode rows than max_requests");
   // Split-KV for chunk tiles (one CTA per SM: K2 holds 512 TMEM columns):
   // key ranges of at most `per` keys, `per` ~ the whole (tile, head) key work
-  // spread over the SMs, at least 512 keys, aligned to K2's key tile.
+  // spread over the SMs, at least two key tiles, aligned to K2's key tile.
   std::vector<TileDesc> items;
   std::vector<CombineDesc> combines;
   {
@@ -942,7 +942,8 @@ void Impl::consume(const isim_batch_plan& p) {
     const int bn = chunk_attention_key_tile(spec_.head_dim());
     std::int64_t work = 0;
     for (const TileDesc& t : tiles) work += static_cast<std::int64_t>(t.pos0 + t.nrows) * H;
-    std::int64_t per = std::max<std::int64_t>(512, (work + 147) / 148);
+    static const int min_keys = getenv("IB2_K2_MIN_KEYS") ? atoi(getenv("IB2_K2_MIN_KEYS")) : 2 * bn;
+    std::int64_t per = std::max<std::int64_t>(min_keys, (work + 147) / 148);
     per = (per + bn - 1) / bn * bn;
     int parts = 0;
     for (const TileDesc& t : tiles) {
