@@ -216,34 +216,6 @@ struct SkSmem {
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
 
-__device__ __forceinline__ void epi_one(const GemmArgs& a, int m, int n, float v) {
-  if (a.bias && a.epi != Epi::SwiGluF16) v += __half2float(a.bias[n]);
-  switch (a.epi) {
-    case Epi::StoreF16: a.out[static_cast<std::int64_t>(m) * a.ldo + n] = __float2half_rn(v); break;
-    case Epi::GeluF16: a.out[static_cast<std::int64_t>(m) * a.ldo + n] = __float2half_rn(gelu_tanh(v)); break;
-    case Epi::ResidAdd: {
-      const std::int64_t i = static_cast<std::int64_t>(m) * a.ldf + n;
-      const float r = a.outf[i] + v;
-      a.outf[i] = a.addf ? r + a.addf[i] : r;
-      break;
-    }
-    case Epi::StoreF32: a.outf[static_cast<std::int64_t>(m) * a.ldf + n] = v; break;
-    default: break;
-  }
-}
-
-// Epilogue of weight row n (this lane) for token m; SwiGLU pairs come from
-// the neighbouring lane (gate = even row, up = odd row).
-__device__ __forceinline__ void epi_row(const GemmArgs& a, int n, int m, float v, int lane) {
-  if (a.epi == Epi::SwiGluF16) {
-    const float up = __shfl_down_sync(0xffffffffu, v, 1);
-    if (!(lane & 1) && m < a.M && n < a.N)
-      a.out[static_cast<std::int64_t>(m) * a.ldo + n / 2] = __float2half_rn(silu(v) * up);
-    return;
-  }
-  if (m < a.M && n < a.N) epi_one(a, m, n, v);
-}
-
 // Epilogue of weight row n (this lane) for tokens m0..m0+15: every global
 // load is issued before any store so the 16 residual read-modify-writes
 // overlap instead of paying one memory latency each.
