@@ -48,10 +48,10 @@ struct AttnCfg {
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BN * HD * 2;  // K or V tile
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
-  static constexpr int P_BYTES = BQ * BN * 2;
+  static constexpr int P_BYTES = BQ * BN * 2;  // one of two P buffers
   static constexpr int KV_OFF = Q_BYTES;
   static constexpr int P_OFF = KV_OFF + STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFF = P_OFF + P_BYTES;
+  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
   static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
   static constexpr int TMEM_COLS = 512;
   static constexpr int S_COL = HD;  // S buffers after O
@@ -73,14 +73,16 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + C::BAR_OFF);
-  std::uint64_t* qfull = bars;                // 1
-  std::uint64_t* kvfull = bars + 1;           // STAGES
-  std::uint64_t* kvempty = kvfull + STAGES;   // STAGES
-  std::uint64_t* sfull = kvempty + STAGES;    // 2
-  std::uint64_t* sfree = sfull + 2;           // 2
-  std::uint64_t* pfull = sfree + 2;           // 1
-  std::uint64_t* pvdone = pfull + 1;          // 1
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(pvdone + 1);
+  std::uint64_t* qfull = bars;              // 1
+  std::uint64_t* kfull = bars + 1;          // [STAGES] K half of a stage landed
+  std::uint64_t* kempty = kfull + STAGES;   // [STAGES] S MMA done with it
+  std::uint64_t* vfull = kempty + STAGES;   // [STAGES] V half landed
+  std::uint64_t* vempty = vfull + STAGES;   // [STAGES] PV MMA done with it
+  std::uint64_t* sfull = vempty + STAGES;   // [2]
+  std::uint64_t* sfree = sfull + 2;         // [2]
+  std::uint64_t* pfull = sfree + 2;         // [2] P buffer written (4 warps)
+  std::uint64_t* pvdone = pfull + 2;        // [2] PV MMA of that P buffer done
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(pvdone + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y;
@@ -90,15 +92,17 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
     prefetch_map(&map_kv);
     mbar_init(qfull, 1);
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&kvfull[i], 1);
-      mbar_init(&kvempty[i], 1);
+      mbar_init(&kfull[i], 1);
+      mbar_init(&kempty[i], 1);
+      mbar_init(&vfull[i], 1);
+      mbar_init(&vempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sfull[i], 1);
       mbar_init(&sfree[i], 4);  // one arrival per softmax warp
+      mbar_init(&pfull[i], 4);
+      mbar_init(&pvdone[i], 1);
     }
-    mbar_init(pfull, 4);
-    mbar_init(pvdone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::TMEM_COLS);
@@ -108,6 +112,8 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
   const std::uint32_t tmem = *tmem_slot;
   pdl_trigger();
   pdl_wait();  // qkv, pool and block tables come from earlier kernels of this iteration
+  items = after_wait(items);
+  table = after_wait(table);
 
   const TileDesc td = items[blockIdx.x];
   const int last_pos = td.pos0 + td.nrows - 1;
@@ -125,26 +131,29 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
       for (int j = 0; j < NCH; ++j) tma_load_2d(sQ + j * BQ * 128, &map_q, qfull, h * HD + 64 * j, td.row0);
       const std::int32_t* tab = table + static_cast<std::int64_t>(td.slot) * max_lb;
       const int lb_last = (kv_hi - 1) / kBlockTokens;
-      for (int t = 0; t < nt; ++t) {
+      // K runs one tile ahead of V: K(t) is released by S(t), V(t) only by PV(t).
+      auto load = [&](int t, int kv) {
         const int st = t % STAGES;
-        if (t >= STAGES) mbar_wait(&kvempty[st], ((t / STAGES) - 1) & 1);
-        mbar_expect_tx(&kvfull[st], C::STAGE_BYTES);
-        unsigned char* sK = sKV + st * C::STAGE_BYTES;
-        unsigned char* sV = sK + C::KV_BYTES;
+        std::uint64_t* full = kv ? &vfull[st] : &kfull[st];
+        if (t >= STAGES) mbar_wait(kv ? &vempty[st] : &kempty[st], ((t / STAGES) - 1) & 1);
+        mbar_expect_tx(full, C::KV_BYTES);
+        unsigned char* dst = sKV + st * C::STAGE_BYTES + kv * C::KV_BYTES;
 #pragma unroll 1
         for (int b = 0; b < BN / kBlockTokens; ++b) {
           // Blocks past the key range re-load the last valid block (finite
           // values; their scores are masked to -inf, so P = 0 there).
           const int lb = min((kt0 + t) * (BN / kBlockTokens) + b, lb_last);
           const std::int64_t pb = tab[lb];
-          const int krow = static_cast<int>(layer_row0 + (pb * 2) * H * kBlockTokens + h * kBlockTokens);
-          const int vrow = krow + H * kBlockTokens;
+          const int row = static_cast<int>(layer_row0 + (pb * 2 + kv) * H * kBlockTokens + h * kBlockTokens);
 #pragma unroll
-          for (int j = 0; j < NCH; ++j) {
-            tma_load_2d(sK + j * BN * 128 + b * kBlockTokens * 128, &map_kv, &kvfull[st], 64 * j, krow);
-            tma_load_2d(sV + j * BN * 128 + b * kBlockTokens * 128, &map_kv, &kvfull[st], 64 * j, vrow);
-          }
+          for (int j = 0; j < NCH; ++j)
+            tma_load_2d(dst + j * BN * 128 + b * kBlockTokens * 128, &map_kv, full, 64 * j, row);
         }
+      };
+      load(0, 0);
+      for (int t = 0; t < nt; ++t) {
+        if (t + 1 < nt) load(t + 1, 0);
+        load(t, 1);
       }
     }
   } else if (warp == 1) {
@@ -153,22 +162,25 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
       constexpr std::uint32_t idesc_pv = idesc_f16(BQ, HD, false, true);
       const std::uint32_t q_base = su32(sQ), kv_base = su32(sKV), p_base = su32(sP);
       auto issue_pv = [&](int u) {
-        mbar_wait(pfull, u & 1);
+        const int pb = u & 1, st = u % STAGES;
+        mbar_wait(&pfull[pb], (u / 2) & 1);
+        mbar_wait(&vfull[st], (u / STAGES) & 1);
         fence_after();
-        const std::uint32_t v_base = kv_base + (u % STAGES) * C::STAGE_BYTES + C::KV_BYTES;
+        const std::uint32_t v_base = kv_base + st * C::STAGE_BYTES + C::KV_BYTES;
+        const std::uint32_t pbuf = p_base + pb * C::P_BYTES;
 #pragma unroll
         for (int k = 0; k < BN / 16; ++k) {
-          const std::uint64_t da = desc_sw128(p_base + (k / 4) * BQ * 128 + (k % 4) * 32, 16, 1024);
+          const std::uint64_t da = desc_sw128(pbuf + (k / 4) * BQ * 128 + (k % 4) * 32, 16, 1024);
           const std::uint64_t db = desc_sw128(v_base + k * 16 * 128, BN * 128, 1024);
           mma_f16(tmem, da, db, idesc_pv, (u > 0 || k > 0) ? 1u : 0u);
         }
-        mma_commit(pvdone);
-        mma_commit(&kvempty[u % STAGES]);
+        mma_commit(&pvdone[pb]);
+        mma_commit(&vempty[st]);
       };
       mbar_wait(qfull, 0);
       for (int t = 0; t < nt; ++t) {
         const int st = t % STAGES, b = t & 1;
-        mbar_wait(&kvfull[st], (t / STAGES) & 1);
+        mbar_wait(&kfull[st], (t / STAGES) & 1);
         if (t >= 2) mbar_wait(&sfree[b], ((t / 2) - 1) & 1);
         fence_after();
         const std::uint32_t k_base = kv_base + st * C::STAGE_BYTES;
@@ -179,6 +191,7 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
           mma_f16(tmem + C::S_COL + b * BN, da, db, idesc_s, k > 0 ? 1u : 0u);
         }
         mma_commit(&sfull[b]);
+        mma_commit(&kempty[st]);
         if (t >= 1) issue_pv(t - 1);
       }
       issue_pv(nt - 1);
@@ -241,25 +254,27 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
         l += back.x + back.y;
         pk[i / 2] = *reinterpret_cast<const std::uint32_t*>(&hv);
       }
-      // P buffer and O are free once PV(t-1) retired.
-      if (t >= 1) {
-        mbar_wait(pvdone, (t - 1) & 1);
+      // P buffer t&1 is free once PV(t-2) retired; O may only be rescaled
+      // after PV(t-1) (which accumulates into it) and before PV(t).
+      const int pbuf = t & 1;
+      if (t >= 2) mbar_wait(&pvdone[pbuf], ((t - 2) / 2) & 1);
+      if (__any_sync(0xffffffffu, rescale)) {
+        if (t >= 1) mbar_wait(&pvdone[(t - 1) & 1], ((t - 1) / 2) & 1);
         fence_after();
-        if (__any_sync(0xffffffffu, rescale)) {
 #pragma unroll 1
-          for (int c = 0; c < HD; c += 16) {
-            std::uint32_t o[16];
-            tmem_ld16_nowait(tmem + lane_off + c, o);
-            tmem_wait_ld();
+        for (int c = 0; c < HD; c += 16) {
+          std::uint32_t o[16];
+          tmem_ld16_nowait(tmem + lane_off + c, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-            tmem_st16(tmem + lane_off + c, o);
-          }
-          tmem_wait_st();
+          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+          tmem_st16(tmem + lane_off + c, o);
         }
+        tmem_wait_st();
       }
       // P row -> shared memory, K-major 128 B swizzle: 16 B unit u of row r
       // lands at unit u ^ (r & 7) of the row's 128 B line.
+      unsigned char* pdst = sP + pbuf * C::P_BYTES;
 #pragma unroll
       for (int u = 0; u < BN / 8; ++u) {
         const int ch = u / 8, uu = u % 8;
@@ -268,15 +283,15 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
         v.y = pk[u * 4 + 1];
         v.z = pk[u * 4 + 2];
         v.w = pk[u * 4 + 3];
-        *reinterpret_cast<uint4*>(sP + ch * BQ * 128 + r * 128 + ((uu ^ (r & 7)) * 16)) = v;
+        *reinterpret_cast<uint4*>(pdst + ch * BQ * 128 + r * 128 + ((uu ^ (r & 7)) * 16)) = v;
       }
       fence_proxy_async();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pfull);
+      if (lane == 0) mbar_arrive(&pfull[pbuf]);
     }
     // Epilogue.
-    mbar_wait(pvdone, (nt - 1) & 1);
+    mbar_wait(&pvdone[(nt - 1) & 1], ((nt - 1) / 2) & 1);
     fence_after();
     if (td.part < 0) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
