@@ -37,6 +37,12 @@ namespace {
 using namespace tc;
 
 constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O when the max grew by > 2^8
 
 template <int HD>
@@ -223,12 +229,20 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
 
       const int k0 = (kt0 + t) * BN;
       float mx = -FLT_MAX;
+      if (k0 >= td.kv_lo && k0 + BN <= kv_hi && k0 + BN - 1 <= qp) {  // whole tile visible to this row
 #pragma unroll
-      for (int i = 0; i < BN; ++i) {
-        const int kp = k0 + i;
-        const bool ok = kp >= td.kv_lo && kp < kv_hi && kp <= qp;
-        s[i] = ok ? s[i] * sc : -FLT_MAX;
-        mx = fmaxf(mx, s[i]);
+        for (int i = 0; i < BN; ++i) {
+          s[i] *= sc;
+          mx = fmaxf(mx, s[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < BN; ++i) {
+          const int kp = k0 + i;
+          const bool ok = kp >= td.kv_lo && kp < kv_hi && kp <= qp;
+          s[i] = ok ? s[i] * sc : -FLT_MAX;
+          mx = fmaxf(mx, s[i]);
+        }
       }
       float factor = 1.f;
       bool rescale = false;
@@ -245,10 +259,14 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
       // P = exp2(s - m_used) rounded to f16; the row sum uses the same rounded
       // values so numerator and denominator agree.
       std::uint32_t pk[BN / 2];
+      // ex2.approx.ftz: masked scores (-FLT_MAX) give 0; results below 2^-126
+      // flush to 0, as f16 rounding (smallest subnormal 2^-24) would anyway.
+      // A row with nothing visible yet (m_used = -FLT_MAX) contributes 0.
+      const float mrow = m_used == -FLT_MAX ? FLT_MAX : m_used;
 #pragma unroll
       for (int i = 0; i < BN; i += 2) {
-        const float e0 = s[i] == -FLT_MAX ? 0.f : exp2f(s[i] - m_used);
-        const float e1 = s[i + 1] == -FLT_MAX ? 0.f : exp2f(s[i + 1] - m_used);
+        const float e0 = ex2_approx(s[i] - mrow);
+        const float e1 = ex2_approx(s[i + 1] - mrow);
         const __half2 hv = __floats2half2_rn(e0, e1);
         const float2 back = __half22float2(hv);
         l += back.x + back.y;
