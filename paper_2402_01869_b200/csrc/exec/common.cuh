@@ -157,6 +157,7 @@ struct GemmArgs {
   QkvWrite qkv;        // Epi::QkvRopeKv only
   int no_early_w;      // diagnostics: no weight prefetch before griddepcontrol.wait
   const float* addf;   // Epi::ResidAdd: if set, outf = (outf + acc) + addf (same [M][ldf] layout)
+  std::int64_t a_rows;  // rows addressable from `a` for TMA bounds (0: the executor's buffer capacity)
 };
 
 }  // namespace ib2

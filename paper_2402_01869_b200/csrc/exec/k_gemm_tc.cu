@@ -996,7 +996,7 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
     sp = {force_s, std::max(1, std::min(max_clusters(tc_splitk_kernel<NT, STAGES>, force_s, L::TOTAL), tiles))};
   static const bool verbose = getenv("IB2_SPLIT_VERBOSE") != nullptr;
   if (verbose) fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d\n", a.N, a.K, a.M, sp.S, sp.clusters);
-  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
+  const std::int64_t a_rows = a.a_rows > 0 ? a.a_rows : (g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
   cudaLaunchConfig_t cfg{};
@@ -1031,7 +1031,24 @@ void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
   else if (a.M <= 32) launch_skinny<32, 8>(a, s);
   else if (a.M <= 64) launch_skinny<64, 6>(a, s);
   else if (a.M <= 128) launch_skinny<128, 5>(a, s);
-  else launch_skinny<256, 4>(a, s);
+  else if ((a.N + BM - 1) / BM * 2 <= g_sms && a.epi != Epi::QkvRopeKv) {
+    // Few weight tiles (O-proj, MLP-out) and 129..256 tokens: the NT = 256
+    // variant has no room for split-K partials and would run one CTA per tile
+    // (32 of 148 SMs); two NT = 128 passes re-read the weights but use every SM.
+    const std::int64_t cap = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
+    for (int m0 = 0; m0 < a.M; m0 += 128) {
+      GemmArgs c = a;
+      c.M = std::min(128, a.M - m0);
+      c.a = a.a + static_cast<std::int64_t>(m0) * a.K;
+      if (c.out) c.out = a.out + static_cast<std::int64_t>(m0) * a.ldo;
+      if (c.outf) c.outf = a.outf + static_cast<std::int64_t>(m0) * a.ldf;
+      if (c.addf) c.addf = a.addf + static_cast<std::int64_t>(m0) * a.ldf;
+      c.a_rows = cap - m0;
+      launch_skinny<128, 5>(c, s);
+    }
+  } else {
+    launch_skinny<256, 4>(a, s);
+  }
 }
 
 }  // namespace

@@ -59,7 +59,7 @@ def reference(a, w, epi, bias=None, resid=None):
 # N = 50400 (GPT-J vocabulary) and 1000 exercise masked N tails.
 SHAPES = [(1, 256, 256), (16, 4096, 4096), (37, 768, 256), (128, 1024, 256), (200, 3072, 1024), (256, 4096, 16384),
           (29, 50400, 4096), (300, 512, 4096), (1000, 12288, 4096), (2048, 256, 1024), (513, 16384, 4096),
-          (700, 1000, 512), (61, 1000, 512), (1500, 4096, 16384), (333, 5632, 1024)]
+          (700, 1000, 512), (61, 1000, 512), (1500, 4096, 16384), (333, 5632, 1024), (200, 4096, 4096), (150, 4096, 16384)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
