@@ -1,18 +1,18 @@
-// K3: projection GEMM on 5th-generation tensor cores (sm_100a).
+// K3: projection GEMMs on 5th-generation tensor cores (sm_100a).
 //
 //   C[M][N] = A[M][K] . W[N][K]^T   (f16 in, fp32 accumulate in TMEM)
 //
-// Warp-specialized, one output tile (128 x BN) per CTA:
-//   warp 0      TMA producer: A and W tiles (128 B swizzle) into a STAGES-deep
-//               shared-memory ring guarded by full/empty mbarriers;
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128,
-//               N=BN, K=16) x4 per 64-wide K block, tcgen05.commit frees the
-//               stage; the final commit signals the epilogue;
-//   warp 2      TMEM allocator (BN fp32 columns);
-//   warps 4-7   epilogue: tcgen05.ld 32x32b.x16 from their TMEM lane quarter,
-//               fused bias / GELU / SwiGLU / residual-add / fp32 store.
-// Tensor maps cover the full buffer capacity; TMA zero-fills the K tail and
-// rows past the buffer, and the epilogue masks rows >= M.
+// Two warp-specialised kernels, both fed by TMA (128 B swizzle) through an
+// mbarrier ring, one elected thread issuing tcgen05.mma, accumulators in TMEM
+// drained by four epilogue warps with fused bias / GELU / SwiGLU / residual
+// epilogues:
+//   * tc_splitk_kernel (M <= 256, decode batches): swap-AB, weights on the
+//     UMMA M side, cluster split-K with a DSMEM reduction;
+//   * tc_gemm_pair_kernel (M > 256, chunk batches): CTA pair, cta_group::2,
+//     256x256 tiles, persistent with double-buffered TMEM accumulators.
+// Weights are stored tile-blocked (model.hpp weight_tile_offset): every TMA of
+// a weight tile is one contiguous 16 KB run.  Tensor maps cover the full buffer
+// capacity; TMA zero-fills rows past it and the epilogues mask rows >= M.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -48,137 +48,6 @@ __device__ __forceinline__ std::uint64_t smem_desc(const void* p) {
   d |= static_cast<std::uint64_t>(2) << 61;      // SWIZZLE_128B
   return d;
 }
-
-template <int BN>
-__host__ __device__ constexpr std::uint32_t instr_desc() {
-  return (1u << 4)                                     // D = f32
-         | (0u << 7)                                   // A = f16
-         | (0u << 10)                                  // B = f16
-         | (static_cast<std::uint32_t>(BN >> 3) << 17) // N
-         | (static_cast<std::uint32_t>(BM >> 4) << 24);// M
-}
-
-template <int BN, int STAGES>
-struct TcSmem {
-  static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;  // + alignment slack
-};
-
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                                                         const __grid_constant__ CUtensorMap map_w, GemmArgs args) {
-  using L = TcSmem<BN, STAGES>;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
-  std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + L::BAR_OFF);
-  std::uint64_t* empty = full + STAGES;
-  std::uint64_t* done = empty + STAGES;
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(done + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // M-fastest rasterization: the M tiles that share a weight tile run in the
-  // same wave, so the weight tile is fetched from HBM once and re-read from L2.
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int nk = (args.K + BK - 1) / BK;
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_a)) : "memory");
-    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(su32(tmem_slot)),
-                 "r"(BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const std::uint32_t tmem = *tmem_slot;
-  pdl_trigger();
-  pdl_wait();  // the prologue above overlapped the predecessor kernel
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
-        unsigned char* sa = smem + s * L::STAGE_BYTES;
-        unsigned char* sb = sa + L::A_BYTES;
-        mbar_expect_tx(&full[s], L::STAGE_BYTES);
-        tma_load_2d(sa, &map_a, &full[s], kb * BK, m0);
-        // Tile-blocked weights: rows of 128-row tile t at k block kb start at
-        // physical row (t * nk + kb) * 128; BN = 256 spans two tiles.
-        const int wt = n0 / 128, wr = n0 % 128;
-        tma_load_2d(sb, &map_w, &full[s], 0, (wt * nk + kb) * 128 + wr);
-        if (BN == 256) tma_load_2d(sb + 128 * BK * 2, &map_w, &full[s], 0, ((wt + 1) * nk + kb) * 128);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr std::uint32_t idesc = instr_desc<BN>();
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        mbar_wait(&full[s], (kb / STAGES) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const unsigned char* sa = smem + s * L::STAGE_BYTES;
-        const std::uint64_t da = smem_desc(sa), db = smem_desc(sa + L::A_BYTES);
-#pragma unroll
-        for (int k = 0; k < BK / UMMA_K; ++k) {
-          const std::uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-          // +32 bytes per 16-element K step inside the 128-byte swizzle atom.
-          asm volatile(
-              "{\n"
-              ".reg .pred p;\n"
-              "setp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-              "}\n" ::"r"(tmem),
-              "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                         su32(&empty[s]))
-                     : "memory");
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(done))
-                   : "memory");
-    }
-  } else if (warp >= 4) {
-    const int q = warp - 4;  // TMEM lane quarter (warp % 4)
-    mbar_wait(done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const int m = m0 + q * 32 + lane;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      std::uint32_t r[16];
-      const std::uint32_t taddr = tmem + (static_cast<std::uint32_t>(q * 32) << 16) + c;
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      float v[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-      if (n0 + c < args.N) epilogue_store<16>(args, m, n0 + c, v);
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  if (warp == 2) {
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(BN));
-  }
-}
-
 
 // ---- small-M path: swap-AB, cluster split-K ----------------------------------
 //
@@ -885,20 +754,6 @@ const CUtensorMap& cached_wmap(const void* base, std::int64_t N, int K, int box_
 
 std::int64_t g_a_rows_capacity = 0;  // rows of every activation buffer (set by the executor)
 
-template <int BN, int STAGES>
-void launch_tc(const GemmArgs& a, cudaStream_t s) {
-  using L = TcSmem<BN, STAGES>;
-  static bool configured = false;
-  if (!configured) {
-    IB2_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
-    configured = true;
-  }
-  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
-  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, BM);
-  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN == 256 ? 128 : BN);
-  dim3 grid((a.M + BM - 1) / BM, (a.N + BN - 1) / BN);
-  launch_pdl(tc_gemm_kernel<BN, STAGES>, grid, dim3(256), L::TOTAL, s, ma, mw, a);
-}
 
 
 int g_sms = 0;
@@ -1084,19 +939,13 @@ void launch_gemm(const GemmArgs& a_in, cudaStream_t s) {
     launch_skinny_any(a, s);
     return;
   }
-  // Small M is weight-bandwidth bound: narrow N tiles put more SMs on the
-  // weight stream.  Large M uses wide tiles for operand reuse.
-  const std::int64_t tiles128 = static_cast<std::int64_t>((a.N + 127) / 128) * ((a.M + BM - 1) / BM);
-  static const bool no_pair = getenv("IB2_NO_PAIR_GEMM") != nullptr;  // diagnostics: old 1-CTA kernel
+  // M > 256: tensor-core bound, CTA-pair 256x256 tiles.
   if (!g_sms) {
     int dev = 0;
     IB2_CUDA(cudaGetDevice(&dev));
     IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  if (!no_pair) launch_tc_pair(a, s);
-  else if (a.M > 512 && a.N >= 1024) launch_tc<256, 4>(a, s);
-  else if (tiles128 >= 148) launch_tc<128, 6>(a, s);
-  else launch_tc<64, 8>(a, s);
+  launch_tc_pair(a, s);
 }
 
 void debug_tile_weights(const void* src, void* dst, int N, int K, void* stream) {
