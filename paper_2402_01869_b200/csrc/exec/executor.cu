@@ -120,8 +120,18 @@ class Impl final : public B200Executor {
   std::int32_t block_table(std::int64_t request_id, std::int32_t* out, std::int32_t cap) const override;
   std::int64_t free_blocks() const override;
   void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out, std::int64_t cap) const override;
+  bool measure_steps() override {
+    step_clock_ = true;
+    return true;
+  }
+  double take_step_seconds() override;
 
  private:
+  // Measured clocks (scheduler Clock::Device / Wall): start / end events of
+  // every consume() on the compute stream since the last take_step_seconds().
+  bool step_clock_ = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> clk_pending_;
+  std::int64_t last_iteration_ = -1;
   struct Touch {
     std::int32_t slot, lb;
     bool was_mapped;
@@ -896,6 +906,10 @@ void Impl::consume(const isim_batch_plan& p) {
     ~ConsumeTimer() { acc += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
   } consume_timer{consume_t0, host_consume_s_};
   IB2_CUDA(cudaSetDevice(dev_));
+  if (step_clock_) {
+    clk_pending_.push_back({new_timing_event(), new_timing_event()});
+    IB2_CUDA(cudaEventRecord(clk_pending_.back().first, main_));
+  }
   retire_host_memory(false);
   if (trace_iters_) {
     iter_mark(0);
@@ -1069,8 +1083,12 @@ void Impl::consume(const isim_batch_plan& p) {
     }
   }
 
+  if (step_clock_) IB2_CUDA(cudaEventRecord(clk_pending_.back().second, main_));
+
   // ---- stats / record ------------------------------------------------------------
-  iters_ += 1;
+  // (measured clocks send one iteration as two plans: forward, then post-phase ops)
+  if (p.iteration != last_iteration_) iters_ += 1;
+  last_iteration_ = p.iteration;
   rows_total_ += n_rows;
   decode_rows_total_ += static_cast<std::int64_t>(drows.size());
   chunk_rows_total_ += n_rows - static_cast<std::int64_t>(drows.size());
@@ -1089,6 +1107,7 @@ void Impl::consume(const isim_batch_plan& p) {
     IB2_CUDA(cudaStreamSynchronize(copy_in_));
     IB2_CUDA(cudaStreamSynchronize(main_));
     check_error();
+    if (step_clock_ && p.n_spans == 0) return;  // post-phase half: keep the forward's outputs
     last_tok_.assign(p.n_spans, -1);
     std::vector<std::int32_t> toks(samples.size());
     if (!samples.empty())
@@ -1287,6 +1306,21 @@ cudaEvent_t Impl::new_timing_event() {
   cudaEvent_t e = spare.back();
   spare.pop_back();
   return e;
+}
+
+double Impl::take_step_seconds() {
+  IB2_CUDA(cudaSetDevice(dev_));
+  if (clk_pending_.empty()) return 0.0;
+  IB2_CUDA(cudaEventSynchronize(clk_pending_.back().second));
+  double ms = 0.0;
+  for (const auto& [a, b] : clk_pending_) {
+    float t = 0.f;
+    IB2_CUDA(cudaEventElapsedTime(&t, a, b));
+    ms += t;
+    ev_free_.push_back({a, b});
+  }
+  clk_pending_.clear();
+  return ms * 1e-3;
 }
 
 double Impl::timer(int op) {

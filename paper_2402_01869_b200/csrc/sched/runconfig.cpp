@@ -1,6 +1,6 @@
 // run_json parsing: the reference keys (proj/src/config.cpp:88-125, including
 // the undocumented "profiled_means") plus this framework's additions
-// ("plan_log", "executor", "exec").  Unknown keys are ignored, as before.
+// ("plan_log", "executor", "exec", "clock").  Unknown keys are ignored, as before.
 #include <json.hpp>
 
 #include "base.hpp"
@@ -36,6 +36,13 @@ RunConfig parse_run_json(const std::string& text) {
     if (j.contains("heuristic_threshold")) c.policy.heuristic_threshold = j["heuristic_threshold"].get<double>();
     if (j.contains("profiled_means"))
       for (const auto& [kind, v] : j["profiled_means"].items()) c.profiled_means[kind] = v.get<double>();
+    if (j.contains("clock")) {
+      const std::string k = j["clock"].get<std::string>();
+      if (k == "virtual") c.clock = Clock::Virtual;
+      else if (k == "device") c.clock = Clock::Device;
+      else if (k == "wall") c.clock = Clock::Wall;
+      else throw ConfigError("run JSON: unknown clock " + k);
+    }
     if (j.contains("plan_log")) c.plan_log = j["plan_log"].get<std::string>();
     if (j.contains("executor")) c.executor = j["executor"].get<std::string>();
     if (c.executor != "none" && c.executor != "b200") throw ConfigError("run JSON: unknown executor " + c.executor);

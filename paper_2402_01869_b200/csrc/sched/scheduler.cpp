@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <thread>
 
 #include <json.hpp>
 
@@ -96,6 +97,13 @@ Scheduler::Scheduler(const std::vector<Request>& trace, const CostModel& model, 
     plans_out_ = std::make_unique<std::ofstream>(cfg_.plan_log);
     if (!*plans_out_) throw IoError("cannot open " + cfg_.plan_log + " for writing");
   }
+  if (cfg_.clock != Clock::Virtual && !(sink_ && sink_->measure_steps()))
+    throw ConfigError("run JSON: a measured clock (\"device\", \"wall\") needs the b200 executor");
+  wall0_ = std::chrono::steady_clock::now();
+}
+
+double Scheduler::wall_seconds() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0_).count();
 }
 
 Scheduler::~Scheduler() = default;
@@ -290,6 +298,10 @@ bool Scheduler::jump_idle() {  // engine.cpp:145-163
     throw SimError("no runnable work and no pending events; request " + who + " cannot fit in GPU KV capacity");
   }
   rep_.waste.preserve += paused_gpu_bytes() * (next - now_);
+  if (cfg_.clock == Clock::Wall) {  // online serving: wait for the event
+    const double wait = next - (wall_seconds() + wall_offset_);
+    if (wait > 0.0) std::this_thread::sleep_for(std::chrono::duration<double>(wait));
+  }
   now_ = next;
   return true;
 }
@@ -570,7 +582,16 @@ bool Scheduler::advance() {
 
   // The model step.  The virtual clock keeps the reference's analytic cost so
   // schedules stay bit-exact; the executor runs the real forward for the plan.
-  const double d_fwd = model_.t_fwd(static_cast<double>(batch_tokens));
+  // Measured clocks (f2) send the phase-0 ops and rows now, wait for the
+  // forward, and advance by the measured time instead.
+  const double d_model = model_.t_fwd(static_cast<double>(batch_tokens));
+  double d_fwd = d_model;
+  if (cfg_.clock != Clock::Virtual) {
+    send_forward();
+    const double dev = sink_->take_step_seconds();
+    if (cfg_.clock == Clock::Device) d_fwd = dev;
+    else d_fwd = std::max(0.0, wall_seconds() + wall_offset_ - now_);
+  }
   now_ += d_fwd + stall;
 
   // Token effects at the iteration boundary (463-481).
@@ -596,6 +617,7 @@ bool Scheduler::advance() {
   double fire_stall = 0.0;
   dispose(fired, static_cast<std::int64_t>(decodes.size()), limit - used_in, &used_out, &fire_stall);
   now_ += fire_stall;
+  if (cfg_.clock == Clock::Wall) wall_offset_ += stall + fire_stall;
   const double d_total = d_fwd + stall + fire_stall;
 
   // Realized waste (489-526).
@@ -611,7 +633,7 @@ bool Scheduler::advance() {
     }
   }
   if (recompute_tokens > 0) {
-    const double added = d_fwd - model_.t_fwd(static_cast<double>(batch_tokens - recompute_tokens));
+    const double added = d_model - model_.t_fwd(static_cast<double>(batch_tokens - recompute_tokens));
     double others = 0.0;
     for (const auto& [key, i] : running_)
       if (std::find(recompute_ids.begin(), recompute_ids.end(), i) == recompute_ids.end())
@@ -653,10 +675,12 @@ void Scheduler::emit_plan(const IterationStat& rec) {
   p.swap_in_tokens = rec.swap_in;
   p.swap_out_tokens = rec.swap_out;
   p.recompute_tokens = rec.recompute_tokens;
-  p.n_ops = static_cast<std::int32_t>(ops_.size());
-  p.n_spans = static_cast<std::int32_t>(spans_.size());
-  p.ops = ops_.data();
-  p.spans = spans_.data();
+  // Measured clocks already sent the phase-0 ops and the rows (send_forward).
+  const std::size_t s0 = spans_sent_ ? spans_.size() : 0;
+  p.n_ops = static_cast<std::int32_t>(ops_.size() - ops_sent_);
+  p.n_spans = static_cast<std::int32_t>(spans_.size() - s0);
+  p.ops = ops_.data() + ops_sent_;
+  p.spans = spans_.data() + s0;
   if (plans_out_) {
     nlohmann::json j;
     j["it"] = rec.index;
@@ -670,9 +694,27 @@ void Scheduler::emit_plan(const IterationStat& rec) {
     j["spans"] = std::move(sp);
     (*plans_out_) << j.dump() << '\n';
   }
-  if (sink_) sink_->consume(p);
+  if (sink_ && (!spans_sent_ || p.n_ops > 0)) sink_->consume(p);
   ops_.clear();
   spans_.clear();
+  ops_sent_ = 0;
+  spans_sent_ = false;
+}
+
+void Scheduler::send_forward() {
+  isim_batch_plan p;
+  p.iteration = iter_ + 1;
+  p.t_end = now_;
+  p.batch_tokens = 0;
+  for (const auto& sp : spans_) p.batch_tokens += sp.count;
+  p.swap_in_tokens = p.swap_out_tokens = p.recompute_tokens = 0;
+  p.n_ops = static_cast<std::int32_t>(ops_.size());
+  p.n_spans = static_cast<std::int32_t>(spans_.size());
+  p.ops = ops_.data();
+  p.spans = spans_.data();
+  sink_->consume(p);
+  ops_sent_ = ops_.size();
+  spans_sent_ = true;
 }
 
 void Scheduler::verify() const {  // engine.cpp:550-565

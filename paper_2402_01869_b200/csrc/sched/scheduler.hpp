@@ -10,6 +10,7 @@
 // point the reference only charged t_fwd (engine.cpp:460).
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <fstream>
 #include <memory>
@@ -28,7 +29,21 @@
 
 namespace ib2 {
 
+// What advances the scheduler's clock each iteration.
+//   Virtual: CostModel::t_fwd(B), the reference's charge (engine.cpp:460);
+//            schedules are bit-exact with the reference.
+//   Device:  the executor's measured device time of the iteration (the step
+//            synchronises); idle periods still jump to the next event.
+//   Wall:    real elapsed seconds since the run started (host + device);
+//            idle periods sleep until the next arrival / API return, so
+//            API calls are timed by the wall clock (online serving).
+// Both measured clocks keep the model's charges for what the GPU does not
+// execute (NaiveSwap stalls) and for the marginal recompute cost in the
+// waste accounting.
+enum class Clock { Virtual, Device, Wall };
+
 struct RunConfig {
+  Clock clock = Clock::Virtual;
   Policy policy = Policy::named(PolicyKind::InferCept);
   Estimator estimator = Estimator::Oracle;
   double max_sim_seconds = 86400.0;
@@ -48,6 +63,11 @@ class PlanSink {
  public:
   virtual ~PlanSink() = default;
   virtual void consume(const isim_batch_plan& plan) = 0;
+  // Measured clocks: enable per-consume device timing; false if unsupported.
+  virtual bool measure_steps() { return false; }
+  // Device seconds of the work enqueued by consume() since the previous call,
+  // returned once that work has completed.
+  virtual double take_step_seconds() { return -1.0; }
 };
 
 // Sorted disjoint [lo,hi) position ranges of one request in one location.
@@ -130,6 +150,8 @@ class Scheduler {
   void record(const Live& s, int kind, std::int64_t lo, std::int64_t hi);
   void add_span(const Live& s, std::int64_t pos, std::int64_t count, int kind, bool sample);
   void emit_plan(const IterationStat& rec);
+  void send_forward();        // measured clocks: phase-0 ops + rows, run now
+  double wall_seconds() const;
 
   const std::vector<Request>& trace_;
   const CostModel& model_;
@@ -155,6 +177,10 @@ class Scheduler {
   std::vector<isim_kv_op> ops_;
   std::vector<isim_row_span> spans_;
   std::int64_t decode_rows_ = 0, batch_tokens_total_ = 0, swapped_total_ = 0;
+  std::size_t ops_sent_ = 0;  // measured clocks: ops_/spans_ already sent
+  bool spans_sent_ = false;
+  std::chrono::steady_clock::time_point wall0_;
+  double wall_offset_ = 0.0;  // wall clock: virtual stall seconds added
 };
 
 }  // namespace ib2

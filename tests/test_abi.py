@@ -61,3 +61,25 @@ def test_executor_without_gpu_fails_loudly():
         assert e.status == 10  # ISIM_ERR_DEVICE, never a silent CPU fallback
     else:
         raise AssertionError("executor created without a GPU")
+
+
+def test_measured_clock_needs_the_executor_and_unknown_clock_is_config_error():
+    # run_json "clock" (f2): "virtual" (default, reference parity), "device",
+    # "wall".  A measured clock without the B200 executor is a config error,
+    # never a silent fallback to the virtual clock.
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from conftest import C0_COST, C0_WORKLOAD
+    import paper_2402_01869_b200 as ib
+    t = ib.Trace.generate(dict(C0_WORKLOAD, request_count=4))
+    m = ib.CostModel.from_json(C0_COST)
+    a = ib.run(t, m, dict(policy="infercept")).summary()
+    assert ib.run(t, m, dict(policy="infercept", clock="virtual")).summary() == a
+    for bad, text in ((dict(clock="device"), "needs the b200 executor"), (dict(clock="wall"), "needs the b200"),
+                      (dict(clock="sundial"), "unknown clock")):
+        try:
+            ib.run(t, m, bad)
+        except ib.IsimError as e:
+            assert e.status == 2 and text in str(e), (bad, e)
+        else:
+            raise AssertionError(f"{bad} accepted")
