@@ -51,7 +51,7 @@ CONFIGS = {
     "C4": dict(model={"preset": "vicuna-13b"}, M=M13,
                workload=dict(classes=ALL6, request_count=4000, arrival_rate=1000.0, seed=23),
                cost=dict(mem_per_token=M13, gpu_kv_capacity=140e9, cpu_kv_capacity=64e9, swap_per_token=M13 / LINK),
-               fast_forward=2000),
+               fast_forward=2000, slack_blocks=64),  # 140 GB pool + 26 GB weights: little room for slack
 }
 
 
@@ -59,7 +59,9 @@ def run_config(name, c, steps, host_gb, link, torch):
     import paper_2402_01869_b200 as ib
     trace = ib.Trace.generate(c["workload"])
     cost = ib.CostModel.from_json(c["cost"])
-    blocks = int(c["cost"]["gpu_kv_capacity"] // (16 * c["M"])) + 512
+    # Ledger capacity in blocks + slack (the Oracle estimator keeps every
+    # request's GPU positions a prefix, so the ledger's blocks suffice).
+    blocks = int(c["cost"]["gpu_kv_capacity"] // (16 * c["M"])) + c.get("slack_blocks", 512)
     pools = dict(gpu_blocks=blocks, host_bytes=int(host_gb * 1e9), max_requests=1024, max_rows=4096, timing=True,
                  stage_tokens=1024, swap_slots=10)
     ex = ib.Executor(c["model"], 0, pools)
