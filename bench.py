@@ -348,17 +348,20 @@ def run_reference(args):
     sess = ib.Session(ib.Trace.generate(WORKLOAD), ib.CostModel.from_json(COST), {"policy": "infercept"})
     sess.step(args.fast_forward + args.warmup)
     c0 = sess.counters()
-    sess.step(args.steps)
+    # Completions per iteration of the schedule (cheap: scheduler only), over
+    # at least 1000 iterations so a short --steps still sees completions.
+    n_sched = max(args.steps, 1000)
+    sess.step(n_sched)
     c1 = sess.counters()
-    per_iter_completed = (c1["completed"] - c0["completed"]) / args.steps
+    per_iter_completed = (c1["completed"] - c0["completed"]) / n_sched
     per_iter, detail = cpu_forward_sample(plans, 3)
     per_iter += (sched_us or 0.0) / 1e6
     value = per_iter_completed / per_iter
     line = {
-        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": per_iter * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "fp32 (numpy)", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD_NAME},
+        "config": {"workload": WORKLOAD_NAME, "host": "rank 0 only, host cores (no GPU used)"},
         "cpu_baseline": {"value": value, "unit": "req/s", "cores": os.cpu_count(), "kind": "port",
                          "sample": (f"reference scheduler (oracle/_ref, {sched_us:.2f} us/iteration, whole trace) + "
                                     f"numpy oracle forward of 3 window iterations (1/2-layer runs "
