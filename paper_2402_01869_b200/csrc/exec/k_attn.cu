@@ -30,8 +30,11 @@ __device__ __forceinline__ void h8_to_f32(const uint4& u, float* f) {
   }
 }
 
+// Occupancy: at head_dim 256 the unconstrained kernel takes 96 registers (5
+// CTAs per SM); capping it at 80 (6 CTAs per SM, 28 B of spills) measured
+// +2 % K1 bandwidth on the C1 window, a cap of 7 CTAs -4 % (profiles/r1j).
 template <int HD>
-__global__ void __launch_bounds__(kDecWarps * 32) decode_attn_kernel(
+__global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn_kernel(
     const f16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
     const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
     const std::int32_t* __restrict__ table, int max_lb, int H, int max_splits, float* __restrict__ part_o,
