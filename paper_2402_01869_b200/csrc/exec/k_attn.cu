@@ -4,7 +4,8 @@
 // scores up to kSplit positions of one (row, head) with 16-byte vector loads
 // of the head's contiguous [16][hd] slice of each paged block (lanes of a
 // token group own 8 dims each, dot products reduced by warp shuffles), then a
-// second pass accumulates P*V; a combine kernel merges the splits.  HBM bound:
+// second pass accumulates P*V; the last split of a (row, head) to finish
+// merges the splits.  HBM bound:
 // algorithmic bytes = 2 * ctx * hd * 2 per (row, head).
 //
 // K2 (chunk rows) lives in k_attn_chunk.cu (tcgen05 + TMEM + TMA).
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
     const f16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
     const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
     const std::int32_t* __restrict__ table, int max_lb, int H, int max_splits, float* __restrict__ part_o,
-    float* __restrict__ part_ml) {
+    float* __restrict__ part_ml, f16* __restrict__ out, std::int32_t* __restrict__ counters) {
   pdl_trigger();
   pdl_wait();
   constexpr int LPT = HD / 8;   // lanes per token
@@ -155,39 +156,44 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
     part_ml[slot_idx * 2] = mx;
     part_ml[slot_idx * 2 + 1] = l;
   }
-}
 
-__global__ void decode_combine_kernel(const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows, int H,
-                                      int HD, int max_splits, int split_len, const float* __restrict__ part_o,
-                                      const float* __restrict__ part_ml, f16* __restrict__ out) {
-  pdl_trigger();
-  pdl_wait();
-  const int dr = blockIdx.x, h = blockIdx.y;
-  const int r = drow[dr];
-  const int ns = (rows[r].pos + 1 + split_len - 1) / split_len;
-  const std::int64_t base = (static_cast<std::int64_t>(dr) * H + h) * max_splits;
+  // The last split of this (row, head) to finish merges all splits (in split
+  // order, so the result does not depend on which CTA is last) and re-arms
+  // the counter: no separate combine launch, and the merge runs in K1's tail.
+  __shared__ int s_last;
+  const int ns = (ctx + kSplit - 1) / kSplit;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int prev = atomicAdd(&counters[dr * H + h], 1);
+    s_last = prev == ns - 1;
+    if (s_last) counters[dr * H + h] = 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const std::int64_t pb = (static_cast<std::int64_t>(dr) * H + h) * max_splits;
   float M = -FLT_MAX;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
+  for (int sp = 0; sp < ns; ++sp) M = fmaxf(M, __ldcg(&part_ml[(pb + sp) * 2]));
   float L = 0.f;
-  for (int s = 0; s < ns; ++s) L += part_ml[(base + s) * 2 + 1] * exp2f(part_ml[(base + s) * 2] - M);
+  for (int sp = 0; sp < ns; ++sp) L += __ldcg(&part_ml[(pb + sp) * 2 + 1]) * exp2f(__ldcg(&part_ml[(pb + sp) * 2]) - M);
   const float inv = 1.f / L;
   for (int i = threadIdx.x; i < HD; i += blockDim.x) {
     float o = 0.f;
-    for (int s = 0; s < ns; ++s) o += part_o[(base + s) * HD + i] * exp2f(part_ml[(base + s) * 2] - M);
-    out[static_cast<std::int64_t>(r) * H * HD + h * HD + i] = __float2half_rn(o * inv);
+    for (int sp = 0; sp < ns; ++sp) o += __ldcg(&part_o[(pb + sp) * HD + i]) * exp2f(__ldcg(&part_ml[(pb + sp) * 2]) - M);
+    out[static_cast<std::int64_t>(r) * D + h * HD + i] = __float2half_rn(o * inv);
   }
 }
 
 template <int HD>
 void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
-                      int layer, int max_pos1, float* part_o, float* part_ml, f16* out, cudaStream_t s) {
+                      int layer, int max_pos1, float* part_o, float* part_ml, f16* out,
+                      std::int32_t* counters, cudaStream_t s) {
   const int max_splits = (max_pos1 + kSplit - 1) / kSplit;
   dim3 grid(max_splits, g.heads, n);
   launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
-             layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml);
-  IB2_LAUNCH_CHECK();
-  launch_pdl(decode_combine_kernel, dim3(n, g.heads), dim3(HD), 0, s, drow, rows, g.heads, HD, max_splits, kSplit,
-             part_o, part_ml, out);
+             layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml,
+             out, counters);
   IB2_LAUNCH_CHECK();
 }
 
@@ -195,12 +201,12 @@ void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* r
 
 void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
-                             f16* out, cudaStream_t s) {
+                             f16* out, std::int32_t* counters, cudaStream_t s) {
   if (n_drows <= 0) return;
   switch (g.head_dim) {
-    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
-    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
-    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, s); break;
+    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
+    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
+    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
     default: throw DeviceError("unsupported head_dim");
   }
 }
