@@ -1189,7 +1189,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
     }
     launch_decode_attention(qkv_, drows_dev_, rows_dev_, n_drows, g, l, max_pos1_, part_o_, part_ml_, attn_,
                               k1_counters_, main_);
-    if (n_drows) kernel_launches_ += 2;
+    if (n_drows) ++kernel_launches_;
     if (time_k1) {
       IB2_CUDA(cudaEventRecord(e1, main_));
       ev_pending_.push_back({e0, e1});
