@@ -142,6 +142,7 @@ def cpu_forward_sample(plans, n_plans=3):
         for pj in plans[:n_plans]:  # materialize contexts
             for (rid, pos, count, kind, sample) in pj["spans"]:
                 fo._ensure(rid, pos + count + 1)
+        fo._forward_only(plans[0])  # untimed warm-up (first-touch of weights, BLAS threads)
         t = time.perf_counter()
         for pj in plans[:n_plans]:
             fo._forward_only(pj)
