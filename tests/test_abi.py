@@ -83,3 +83,22 @@ def test_measured_clock_needs_the_executor_and_unknown_clock_is_config_error():
             assert e.status == 2 and text in str(e), (bad, e)
         else:
             raise AssertionError(f"{bad} accepted")
+
+
+def test_reference_capi_suite_links_against_product():
+    """Drop-in proof: the reference's own C-API suite (proj/tests/test_capi.cpp:30-136),
+    compiled unchanged, linked against OUR library instead of libinterceptsim.so."""
+    import shutil
+    import subprocess
+    import pytest
+    if not os.path.isdir("/root/reference/proj/tests") and not os.path.exists(
+            os.path.join(ROOT, "oracle", "_ref", "obj", "test_capi.o")):
+        pytest.skip("reference sources absent and no prebuilt test_capi.o")
+    if shutil.which("make") is None:
+        pytest.skip("make absent")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "product-capi"], check=True,
+                   capture_output=True)
+    out = subprocess.run([os.path.join(ROOT, "oracle", "_ref", "capi_tests_product")], capture_output=True,
+                         text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "4 | 4 passed | 0 failed" in out.stdout, out.stdout

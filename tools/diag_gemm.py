@@ -1,7 +1,7 @@
 """Diagnostic (not collected): time the GPT-J decode-step projection GEMMs
 (M tokens, fp16 weights) back to back with CUDA events."""
-import ctypes, sys
-sys.path.insert(0, "/root/repo")
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2402_01869_b200 import _abi
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 32

@@ -1,7 +1,7 @@
 """Diagnostic (not collected): chunk-sized (M = 300..2048) GPT-J projection
 GEMMs, weights rotated over 4 copies; TFLOP/s per shape."""
-import ctypes, sys
-sys.path.insert(0, "/root/repo")
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2402_01869_b200 import _abi
 shapes = {"qkv": (12288, 4096, 0), "o": (4096, 4096, 2), "mlp_in": (16384, 4096, 1), "mlp_out": (4096, 16384, 2)}

@@ -1,6 +1,6 @@
 """Diagnostic (not collected): one GEMM shape, a few launches (for ncu)."""
-import ctypes, sys
-sys.path.insert(0, "/root/repo")
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2402_01869_b200 import _abi
 M, N, K, epi = (int(x) for x in sys.argv[1:5])

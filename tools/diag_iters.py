@@ -2,8 +2,9 @@
 iteration type, split into preamble (swap-in scatters it waits for, block
 tables, swap-in issue), forward, and post phase (swap-out gather, frees) --
 plus how long the host spent inside consume() and blocked on events."""
+import os
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench
 import paper_2402_01869_b200 as ib

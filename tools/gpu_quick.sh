@@ -10,4 +10,4 @@ tail -30 gpurun_out/${TAG}_pytest.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/${TAG}_smoke.log
 timeout 900 python bench.py ${BENCH_ARGS:---no-cpu-baseline} > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"
 cat gpurun_out/${TAG}_bench.json; tail -3 gpurun_out/${TAG}_bench.err
-[ "${DIAG:-1}" = 1 ] && timeout 600 python tests/diag_iters.py 3000 300 > gpurun_out/${TAG}_iters.txt 2>&1; tail -10 gpurun_out/${TAG}_iters.txt
+[ "${DIAG:-1}" = 1 ] && timeout 600 python tools/diag_iters.py 3000 300 > gpurun_out/${TAG}_iters.txt 2>&1; tail -10 gpurun_out/${TAG}_iters.txt
