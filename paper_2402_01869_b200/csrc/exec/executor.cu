@@ -125,6 +125,18 @@ class Impl final : public B200Executor {
     return true;
   }
   double take_step_seconds() override;
+  void check_capacity(std::int64_t ledger_blocks, bool two_runs, int block_size) override {
+    if (block_size != kBlockTokens)
+      throw ConfigError("executor: the cost model's block_size must be " + std::to_string(kBlockTokens));
+    // Oracle / Profiled estimators keep every request's GPU positions a
+    // prefix, so the device needs exactly the ledger's blocks; the Dynamic
+    // estimator can leave two runs per request (at most 2 extra blocks each).
+    const std::int64_t need = ledger_blocks + (two_runs ? 2LL * max_slots_ : 0);
+    if (gpu_blocks_ < need)
+      throw ConfigError("executor: gpu_blocks " + std::to_string(gpu_blocks_) + " < " + std::to_string(need) +
+                        " (ledger capacity in blocks" + (two_runs ? " + 2 per live request for the Dynamic estimator" : "") +
+                        ")");
+  }
 
  private:
   // Measured clocks (scheduler Clock::Device / Wall): start / end events of

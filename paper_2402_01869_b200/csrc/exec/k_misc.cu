@@ -253,6 +253,9 @@ __global__ void gather_rows_kernel(const f16* __restrict__ src, int ld, const st
 
 // K8: single CTA, two phases separated by a barrier so pops may consume the
 // blocks pushed by this launch (LIFO: the last freed block is reused first).
+// A double free or an empty pool is a plan / sizing bug: the kernel records
+// the code and traps, so the launch fails loudly before any later kernel of
+// the iteration could use a -1 block id as a pool offset.
 __global__ void __launch_bounds__(1024) block_update_kernel(std::int32_t* __restrict__ table,
                                                             std::int32_t* __restrict__ stack,
                                                             std::int32_t* __restrict__ top,
@@ -265,7 +268,10 @@ __global__ void __launch_bounds__(1024) block_update_kernel(std::int32_t* __rest
   for (int k = threadIdx.x; k < nf; k += blockDim.x) {
     const int e = frees[k];
     const int pb = table[e];
-    if (pb < 0) atomicExch(err, 1);
+    if (pb < 0) {
+      atomicExch(err, 1);
+      __trap();
+    }
     stack[t0 + k] = pb;
     table[e] = -1;
   }
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(1024) block_update_kernel(std::int32_t* __rest
     const int e = allocs[k];
     if (src < 0 || table[e] >= 0) {
       atomicExch(err, 2);
-      continue;
+      __trap();
     }
     table[e] = stack[src];
   }

@@ -64,6 +64,22 @@ std::vector<std::pair<std::int64_t, std::int64_t>> PosSet::take_all() {
   return out;
 }
 
+std::vector<std::pair<std::int64_t, std::int64_t>> PosSet::take_within(std::int64_t lo, std::int64_t hi) {
+  std::vector<std::pair<std::int64_t, std::int64_t>> out, keep;
+  for (const auto& r : r_) {
+    const std::int64_t a = std::max(lo, r.first), b = std::min(hi, r.second);
+    if (a >= b) {
+      keep.push_back(r);
+      continue;
+    }
+    out.emplace_back(a, b);
+    if (r.first < a) keep.emplace_back(r.first, a);
+    if (b < r.second) keep.emplace_back(b, r.second);
+  }
+  r_.swap(keep);
+  return out;
+}
+
 // ------------------------------------------------------------- Scheduler --
 
 Scheduler::Scheduler(const std::vector<Request>& trace, const CostModel& model, const RunConfig& cfg, PlanSink* sink)
@@ -96,6 +112,11 @@ Scheduler::Scheduler(const std::vector<Request>& trace, const CostModel& model, 
   if (!cfg_.plan_log.empty()) {
     plans_out_ = std::make_unique<std::ofstream>(cfg_.plan_log);
     if (!*plans_out_) throw IoError("cannot open " + cfg_.plan_log + " for writing");
+  }
+  if (sink_) {
+    const double per_block = static_cast<double>(model_.block_size) * model_.mem_per_token;
+    const auto ledger_blocks = static_cast<std::int64_t>(std::floor((model_.gpu_kv_capacity + 0.5) / per_block));
+    sink_->check_capacity(ledger_blocks, cfg_.estimator == Estimator::Dynamic, model_.block_size);
   }
   if (cfg_.clock != Clock::Virtual && !(sink_ && sink_->measure_steps()))
     throw ConfigError("run JSON: a measured clock (\"device\", \"wall\") needs the b200 executor");
@@ -324,6 +345,11 @@ void Scheduler::evict(std::int64_t i) {  // engine.cpp:179-188
   if (events_out_) events_.push_back("evict:" + std::to_string(v.req->id));
   // Rows already batched for the victim this iteration are dropped from the
   // device batch ("ghost decodes"); the scheduler still counts them.
+  // A dropped decode row's input id is already in the history (sampled by an
+  // earlier iteration); a dropped FRESH span's synthetic ids are not, so its
+  // positions are remembered and re-emitted as FRESH when recomputed.
+  for (const auto& sp : spans_)
+    if (sp.request_id == v.req->id && sp.kind == ISIM_SPAN_FRESH) v.unwritten.add(sp.pos, sp.pos + sp.count);
   spans_.erase(std::remove_if(spans_.begin(), spans_.end(),
                               [&](const isim_row_span& sp) { return sp.request_id == v.req->id; }),
                spans_.end());
@@ -352,6 +378,7 @@ void Scheduler::finish_request(std::int64_t i) {  // engine.cpp:204-216
   s.recompute_pending = 0;
   recomputing_.erase(i);
   s.recompute_restored = 0;
+  s.unwritten.take_all();
   op_release(s);
   done_ += 1;
 }
@@ -525,7 +552,13 @@ bool Scheduler::advance() {
       for (const auto& [lo, hi] : ranges) {
         if (left <= 0) break;
         const std::int64_t k = std::min(left, hi - lo);
-        add_span(s, lo, k, ISIM_SPAN_RECOMPUTE, false);
+        std::int64_t at = lo;
+        for (const auto& [a, b] : s.unwritten.take_within(lo, lo + k)) {
+          add_span(s, at, a - at, ISIM_SPAN_RECOMPUTE, false);
+          add_span(s, a, b - a, ISIM_SPAN_FRESH, false);
+          at = b;
+        }
+        add_span(s, at, lo + k - at, ISIM_SPAN_RECOMPUTE, false);
         left -= k;
       }
       if (fresh == 0 && completes && static_cast<std::int64_t>(spans_.size()) > before) spans_.back().sample = 1;

@@ -68,6 +68,11 @@ class PlanSink {
   // Device seconds of the work enqueued by consume() since the previous call,
   // returned once that work has completed.
   virtual double take_step_seconds() { return -1.0; }
+  // Called once before the first plan: the ledger's capacity in 16-token
+  // blocks and whether the position model may hold up to two GPU runs per
+  // request (Dynamic estimator).  A sink with a
+  // physical block pool throws ConfigError if it cannot hold that.
+  virtual void check_capacity(std::int64_t /*ledger_blocks*/, bool /*two_runs*/, int /*block_size*/) {}
 };
 
 // Sorted disjoint [lo,hi) position ranges of one request in one location.
@@ -80,6 +85,8 @@ class PosSet {
   std::vector<std::pair<std::int64_t, std::int64_t>> take_low(std::int64_t n);
   std::vector<std::pair<std::int64_t, std::int64_t>> take_high(std::int64_t n);
   std::vector<std::pair<std::int64_t, std::int64_t>> take_all();
+  // Remove and return the members of [lo,hi), in position order.
+  std::vector<std::pair<std::int64_t, std::int64_t>> take_within(std::int64_t lo, std::int64_t hi);
   const std::vector<std::pair<std::int64_t, std::int64_t>>& ranges() const { return r_; }
 
  private:
@@ -119,6 +126,10 @@ class Scheduler {
     double first_token = -1.0, completion = -1.0;
     std::int64_t output_tokens = 0;
     PosSet gpu, cpu, gone;  // position model
+    // Prompt / API-return positions whose FRESH rows were dropped by an
+    // eviction in the same iteration: their token ids never reached the
+    // device history, so their recompute is emitted as FRESH (synthetic ids).
+    PosSet unwritten;
   };
 
   // queue / lifecycle

@@ -1,0 +1,67 @@
+"""Plan-level invariant: every token id a row reads was produced before it is read.
+
+A FRESH span writes its synthetic ids into the request's history; a sampling
+row at position p writes the greedy id of position p+1; DECODE and RECOMPUTE
+rows read the history.  An eviction inside the API-return loop
+(reference proj/src/engine.cpp:357-386, evict 179-188) drops the victim's
+already-batched FRESH rows from the device batch; their positions must come
+back as FRESH (not RECOMPUTE) when the victim is recomputed, or the device
+would embed ids that were never written.
+"""
+import json
+
+from conftest import C0_COST, C0_WORKLOAD
+
+# Preserve policy on a 12,288-token pool: request 14's API-return chunk
+# [2552, 2563) is grown and then evicted in iteration 4757, and recomputed in
+# iteration 4837 (found by sweeping seeds / pools).
+EVICT_WORKLOAD = dict(C0_WORKLOAD, request_count=32, arrival_rate=2.0, seed=3)
+EVICT_COST = dict(C0_COST, gpu_kv_capacity=12288 * 4096)
+
+
+def unread_positions(plans):
+    known, bad = {}, []
+    for pj in plans:
+        for (rid, pos, count, kind, sample) in pj["spans"]:
+            k = known.setdefault(rid, set())
+            if kind == 1:
+                k.update(range(pos, pos + count))
+            else:
+                miss = [p for p in range(pos, pos + count) if p not in k]
+                if miss:
+                    bad.append((pj["it"], rid, kind, miss[:4], len(miss)))
+            if sample:
+                k.add(pos + count)
+        for (rid, kind, phase, lo, hi) in pj["ops"]:
+            if kind == 5:
+                known.pop(rid, None)
+    return bad
+
+
+def plans_of(workload, cost, cfg, tmp_path):
+    import paper_2402_01869_b200 as ib
+    path = str(tmp_path / "plans.jsonl")
+    ib.run(ib.Trace.generate(workload), ib.CostModel.from_json(cost), dict(cfg, plan_log=path, check_invariants=True))
+    return [json.loads(l) for l in open(path)]
+
+
+def test_c0_history_provenance(c0_plans):
+    plans, _ = c0_plans
+    assert unread_positions(plans) == []
+
+
+def test_evicted_fresh_rows_are_reemitted_as_fresh(tmp_path):
+    plans = plans_of(EVICT_WORKLOAD, EVICT_COST, dict(policy="preserve"), tmp_path)
+    assert unread_positions(plans) == []
+    by_it = {p["it"]: p for p in plans}
+    # iteration 4757: request 14 grows [2552, 2563) and is discarded; no rows run
+    assert [o for o in by_it[4757]["ops"] if o[0] == 14] == [[14, 0, 0, 2552, 2563], [14, 3, 0, 0, 2563]]
+    assert [s for s in by_it[4757]["spans"] if s[0] == 14] == []
+    # iteration 4837: one recompute op, rows split into history ids + synthetic ids
+    assert [s for s in by_it[4837]["spans"] if s[0] == 14] == [[14, 0, 2552, 2, 0], [14, 2552, 11, 1, 1]]
+
+
+def test_dynamic_and_policies_history_provenance(tmp_path):
+    for policy, est in [("infercept", "dynamic"), ("vanilla-discard", "oracle"), ("swap", "oracle")]:
+        plans = plans_of(dict(C0_WORKLOAD, request_count=24), C0_COST, dict(policy=policy, estimator=est), tmp_path)
+        assert unread_positions(plans) == [], (policy, est)
