@@ -12,11 +12,12 @@ import json
 
 from conftest import C0_COST, C0_WORKLOAD
 
-# Preserve policy on a 12,288-token pool: request 14's API-return chunk
-# [2552, 2563) is grown and then evicted in iteration 4757, and recomputed in
-# iteration 4837 (found by sweeping seeds / pools).
-EVICT_WORKLOAD = dict(C0_WORKLOAD, request_count=32, arrival_rate=2.0, seed=3)
-EVICT_COST = dict(C0_COST, gpu_kv_capacity=12288 * 4096)
+# Preserve policy on a 4,096-token pool: request 0's API-return chunk
+# [1258, 1294) is grown and then evicted in iteration 635, and recomputed in
+# iteration 701 (found by sweeping seeds / pools).
+EVICT_WORKLOAD = dict(C0_WORKLOAD, request_count=16, arrival_rate=4.0, seed=12, max_seq_len=2048)
+EVICT_COST = dict(C0_COST, gpu_kv_capacity=4096 * 4096)
+EVICT_AT, RECOMPUTE_AT = 635, 701
 
 
 def unread_positions(plans):
@@ -54,11 +55,11 @@ def test_evicted_fresh_rows_are_reemitted_as_fresh(tmp_path):
     plans = plans_of(EVICT_WORKLOAD, EVICT_COST, dict(policy="preserve"), tmp_path)
     assert unread_positions(plans) == []
     by_it = {p["it"]: p for p in plans}
-    # iteration 4757: request 14 grows [2552, 2563) and is discarded; no rows run
-    assert [o for o in by_it[4757]["ops"] if o[0] == 14] == [[14, 0, 0, 2552, 2563], [14, 3, 0, 0, 2563]]
-    assert [s for s in by_it[4757]["spans"] if s[0] == 14] == []
-    # iteration 4837: one recompute op, rows split into history ids + synthetic ids
-    assert [s for s in by_it[4837]["spans"] if s[0] == 14] == [[14, 0, 2552, 2, 0], [14, 2552, 11, 1, 1]]
+    # iteration 635: request 0 grows [1258, 1294) and is discarded; no rows run
+    assert [o for o in by_it[EVICT_AT]["ops"] if o[0] == 0] == [[0, 0, 0, 1258, 1294], [0, 3, 0, 0, 1294]]
+    assert [s for s in by_it[EVICT_AT]["spans"] if s[0] == 0] == []
+    # iteration 701: one recompute op, rows split into history ids + synthetic ids
+    assert [s for s in by_it[RECOMPUTE_AT]["spans"] if s[0] == 0] == [[0, 0, 1258, 2, 0], [0, 1258, 36, 1, 1]]
 
 
 def test_dynamic_and_policies_history_provenance(tmp_path):
