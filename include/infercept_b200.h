@@ -176,6 +176,13 @@ isim_status isim_session_open(const isim_trace* trace, const isim_model* model, 
                               isim_session** out);
 /* Run up to max_iters scheduler iterations (idle jumps do not count). */
 isim_status isim_session_step(isim_session* s, int64_t max_iters, int64_t* iters_done, int32_t* finished);
+/* Run up to max_iters iterations without the executor (scheduler only,
+ * virtual clock), then hand the executor the KV layout the ledger describes:
+ * every request it held is released first, then each live request's host
+ * positions are grown + swapped out and its GPU positions grown, as plans
+ * without rows.  Decisions are unchanged; KV bytes are not meaningful, so this
+ * positions timing windows (bench), not parity checks. */
+isim_status isim_session_fast_forward(isim_session* s, int64_t max_iters, int64_t* iters_done, int32_t* finished);
 /* Counters since open: completed requests, decode rows, batch tokens. */
 isim_status isim_session_counters(const isim_session* s, int64_t* completed, int64_t* decode_rows,
                                   int64_t* batch_tokens, int64_t* swapped_tokens);

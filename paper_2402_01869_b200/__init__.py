@@ -265,6 +265,14 @@ class Session(_Handle):
         _abi.check(_L.isim_session_step(self._ptr, max_iters, ctypes.byref(done), ctypes.byref(fin)))
         return done.value, bool(fin.value)
 
+    def fast_forward(self, max_iters: int) -> tuple:
+        """Scheduler-only iterations, then the executor is handed the ledger's
+        KV layout (isim_session_fast_forward): positions timing windows."""
+        done = ctypes.c_int64()
+        fin = ctypes.c_int32()
+        _abi.check(_L.isim_session_fast_forward(self._ptr, max_iters, ctypes.byref(done), ctypes.byref(fin)))
+        return done.value, bool(fin.value)
+
     def counters(self) -> dict:
         v = [ctypes.c_int64() for _ in range(4)]
         _abi.check(_L.isim_session_counters(self._ptr, *[ctypes.byref(x) for x in v]))

@@ -1252,6 +1252,7 @@ void Impl::sync() {
   IB2_CUDA(cudaStreamSynchronize(copy_));
   IB2_CUDA(cudaStreamSynchronize(copy_in_));
   check_error();
+  retire_host_memory(true);  // every copy reading a released extent has completed
   for (std::size_t i = 0; i < ev_pending_.size(); ++i) {
     float ms = 0.f;
     IB2_CUDA(cudaEventElapsedTime(&ms, ev_pending_[i].first, ev_pending_[i].second));

@@ -750,6 +750,96 @@ void Scheduler::send_forward() {
   spans_sent_ = true;
 }
 
+void Scheduler::send_ops(std::vector<isim_kv_op>& ops) {
+  if (ops.empty()) return;
+  isim_batch_plan p;
+  p.iteration = iter_;
+  p.t_end = now_;
+  p.batch_tokens = p.swap_in_tokens = p.swap_out_tokens = p.recompute_tokens = 0;
+  p.n_ops = static_cast<std::int32_t>(ops.size());
+  p.n_spans = 0;
+  p.ops = ops.data();
+  p.spans = nullptr;
+  sink_->consume(p);
+  ops.clear();
+}
+
+std::int64_t Scheduler::fast_forward(std::int64_t n, bool* finished) {
+  if (cfg_.clock != Clock::Virtual) throw ConfigError("fast_forward needs the virtual clock");
+  auto live = [](const Live& s) { return s.at != Where::NotArrived && s.at != Where::Completed; };
+  auto make = [](std::int64_t rid, int kind, int phase, std::int64_t lo, std::int64_t hi) {
+    isim_kv_op o;
+    o.request_id = rid;
+    o.kind = kind;
+    o.phase = phase;
+    o.pos_lo = lo;
+    o.pos_hi = hi;
+    return o;
+  };
+  std::vector<isim_kv_op> ops;
+  if (sink_) {
+    // Ops carried over from an idle jump go first, then every request the
+    // sink holds (anything with positions) is released.
+    ops.assign(ops_.begin() + static_cast<std::ptrdiff_t>(ops_sent_), ops_.end());
+    for (const Live& s : st_)
+      if (live(s) && !(s.gpu.empty() && s.cpu.empty() && s.gone.empty()))
+        ops.push_back(make(s.req->id, ISIM_KV_RELEASE, 1, 0, s.gpu.size() + s.cpu.size() + s.gone.size()));
+    send_ops(ops);
+  }
+  ops_.clear();
+  spans_.clear();
+  ops_sent_ = 0;
+  spans_sent_ = false;
+  PlanSink* keep = sink_;
+  sink_ = nullptr;
+  std::int64_t done = 0;
+  bool fin = false;
+  try {
+    while (done < n) {
+      const std::int64_t before = iter_;
+      if (!advance()) {
+        fin = true;
+        break;
+      }
+      done += iter_ - before;
+    }
+  } catch (...) {
+    sink_ = keep;
+    throw;
+  }
+  sink_ = keep;
+  ops_.clear();  // carried ops are reflected in the position sets handed over below
+  if (finished) *finished = fin;
+  if (!sink_) return done;
+  // Hand-over, host positions first while the device pool is empty (each
+  // batch is grown then swapped out, so it only borrows blocks), then every
+  // GPU run in one plan.
+  const std::int64_t batch = 8192;
+  std::int64_t in_batch = 0;
+  std::vector<isim_kv_op> post;
+  for (const Live& s : st_) {
+    if (!live(s) || s.cpu.empty()) continue;
+    for (const auto& [lo, hi] : s.cpu.ranges()) {
+      ops.push_back(make(s.req->id, ISIM_KV_GROW, 0, lo, hi));
+      post.push_back(make(s.req->id, ISIM_KV_SWAP_OUT, 1, lo, hi));
+      in_batch += hi - lo;
+    }
+    if (in_batch >= batch) {
+      ops.insert(ops.end(), post.begin(), post.end());
+      post.clear();
+      send_ops(ops);
+      in_batch = 0;
+    }
+  }
+  ops.insert(ops.end(), post.begin(), post.end());
+  send_ops(ops);
+  for (const Live& s : st_)
+    if (live(s))
+      for (const auto& [lo, hi] : s.gpu.ranges()) ops.push_back(make(s.req->id, ISIM_KV_GROW, 0, lo, hi));
+  send_ops(ops);
+  return done;
+}
+
 void Scheduler::verify() const {  // engine.cpp:550-565
   if (kv_.gpu_bytes() > model_.gpu_kv_capacity + 1.0) throw SimError("GPU capacity invariant violated");
   if (kv_.cpu_bytes() > model_.cpu_kv_capacity + 1.0) throw SimError("CPU capacity invariant violated");

@@ -99,6 +99,15 @@ class Scheduler {
   ~Scheduler();
 
   bool advance();          // one iteration, or one idle jump; false when done
+  // Fast-forward: release every request the sink holds, run up to n
+  // iterations without the sink (scheduler only, virtual clock), then hand
+  // the sink the KV layout the ledger now describes -- each live request's
+  // GPU positions grown in place and its host positions grown and swapped
+  // out -- as plans without rows.  Scheduling is unchanged (the sink never
+  // influences decisions); the sink's KV bytes are whatever the hand-over
+  // wrote, so this serves timing (the bench), not numerics.  Returns the
+  // iterations run.
+  std::int64_t fast_forward(std::int64_t n, bool* finished);
   RunReport conclude();    // engine.cpp:583-601
 
   double now() const { return now_; }
@@ -162,6 +171,7 @@ class Scheduler {
   void add_span(const Live& s, std::int64_t pos, std::int64_t count, int kind, bool sample);
   void emit_plan(const IterationStat& rec);
   void send_forward();        // measured clocks: phase-0 ops + rows, run now
+  void send_ops(std::vector<isim_kv_op>& ops);  // a plan with ops only
   double wall_seconds() const;
 
   const std::vector<Request>& trace_;

@@ -34,7 +34,7 @@ def test_eviction_in_api_return_loop(tmp_path):
     assert unread_positions(plans) == []
     n = RECOMPUTE_AT + 40
     evictions = sum(1 for p in plans[:n] for o in p["ops"] if o[1] == 3)
-    r = replay(plans, {"preset": "tiny"}, pools_for(EVICT_COST, 2048), n,
+    r = replay(plans, {"preset": "tiny"}, pools_for(EVICT_COST, 2048, max_rows=4096), n,
                check_tables_every=5)
     assert evictions > 0 and r["sampled"] > 300
     print("eviction replay", evictions, "discards", {k: v for k, v in r.items() if k != "stats"})

@@ -66,3 +66,19 @@ def test_dynamic_and_policies_history_provenance(tmp_path):
     for policy, est in [("infercept", "dynamic"), ("vanilla-discard", "oracle"), ("swap", "oracle")]:
         plans = plans_of(dict(C0_WORKLOAD, request_count=24), C0_COST, dict(policy=policy, estimator=est), tmp_path)
         assert unread_positions(plans) == [], (policy, est)
+
+
+def test_fast_forward_keeps_the_schedule(tmp_path):
+    """isim_session_fast_forward runs the same iterations as isim_session_step
+    (the sink never influences decisions): identical counters and summary."""
+    import paper_2402_01869_b200 as ib
+    t = ib.Trace.generate(C0_WORKLOAD)
+    m = ib.CostModel.from_json(C0_COST)
+    a = ib.Session(t, m, dict(policy="infercept"))
+    b = ib.Session(t, m, dict(policy="infercept"))
+    for n in (500, 1200, 3000):
+        assert a.step(n) == b.fast_forward(n)
+        assert a.counters() == b.counters()
+    a.step(10 ** 9)
+    b.step(10 ** 9)
+    assert a.finish().summary() == b.finish().summary()
