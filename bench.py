@@ -1,25 +1,41 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 InferCept serving hot path (driver contract).
 
-Workload (BASELINE.json configs[1]): a GPT-J-6B-shaped
-random-init model serving the Math/QA/Chatbot API-augmented trace (2000
-requests @3/s, seed 11) under InferCept's min-waste policy (reference cost
-model defaults, M = 458,752 B/token, 150 GB GPU KV pool, 50 GB/s link).  A
-"step" is one scheduler iteration: the C++ scheduler forms the batch (decode
-rows + API-return / prefill / recompute chunks + budgeted swaps) and the
-executor runs the model step on the paged KV cache.
+Workload (BASELINE.json configs[4], SURVEY §8d C4 -- the largest single-GPU
+configuration and the one the scaling run shards): a Vicuna-13B-shaped
+random-init model serving a fixed 4000-request API-augmented trace (all six
+Table-1 classes, seed 23, arrivals at 1000/s: saturating) under InferCept's
+min-waste policy (reference cost model defaults, M = 819,200 B/token, 140 GB
+GPU / 64 GB CPU KV ledger per replica, 50 GB/s link).  With N GPUs, rank r
+serves the requests with id mod N == r at their original arrival times (its
+own engine, KV pool and pinned host pool; no collective on the data path):
+strong scaling of one fixed trace (reference concurrency
+contract proj/include/interceptsim.h:10-11).
 
-The trace is first fast-forwarded (untimed) to steady state, then W warm-up
-iterations, then exactly K timed iterations.  `value` = requests completed in
-the timed window / device seconds (CUDA events on the executor's stream);
-`e2e` = the same through the public C ABI session with host wall clock,
-including each step's plan H2D upload from pinned memory and the D2H read of
-the sampled token ids.  N > 1 (torchrun): request-sharded replicas (id mod N),
-one per GPU, no collective on the data path; value = sum over ranks / max time.
+A "step" is one scheduler iteration: the C++ scheduler (bit-exact with the
+reference engine, proj/src/engine.cpp:282-548) forms the batch and the
+executor runs the model step at the engine.cpp:460 hook on the paged KV
+cache.
 
---impl reference: the reference's CPU path of this step on the host cores:
-the reference scheduler (oracle/_ref, compiled from /root/reference) plus the
-CPU oracle port of the model step (numpy; bounded sample, extrapolated).
+Estimator (identical in both arms).  The reference's throughput is
+completed / makespan (proj/src/metrics.cpp:41-50).  A replica's schedule is
+deterministic, so its completions C and iteration count I are known from a
+scheduler-only run (cheap, CPU); what is measured is the time per iteration.
+The K timed iterations are spread over n windows centred on evenly spaced
+points of the replica's schedule (a stratified sample of the whole replay;
+each window is reached by a scheduler-only fast-forward, then W untimed
+warm-up iterations on the GPU, then its timed iterations between a barrier
+and device syncs).  value = sum_r C_r / max_r (I_r * mean device s/iteration
+of rank r); e2e the same with host wall seconds through the public C ABI
+session (plan upload from pinned memory and sampled-id read-back included).
+
+--impl reference: the reference's CPU path of the same schedule on this host:
+the reference engine (oracle/_ref, compiled from /root/reference) runs the
+whole trace; its event log with ledger snapshots gives each iteration's batch
+(oracle/ref_plans.py, no product code loaded); the numpy fp32 oracle forward
+(oracle/forward.py) of the sampled iterations, timed with all host threads
+(1- and 2-layer runs, extrapolated to the model's depth), plus the
+reference scheduler's own seconds per iteration, is its time per iteration.
 """
 import argparse
 import json
@@ -35,13 +51,50 @@ sys.path.insert(0, ROOT)
 
 BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
-GPTJ_M = 458752
 LINK = 50e9
-WORKLOAD = dict(classes=[{"name": "Math"}, {"name": "QA"}, {"name": "Chatbot"}], request_count=2000,
-                arrival_rate=3.0, seed=11)
-COST = dict(mem_per_token=GPTJ_M, gpu_kv_capacity=150e9, cpu_kv_capacity=128e9, swap_per_token=GPTJ_M / LINK)
-WORKLOAD_NAME = ("C1: GPT-J-6B-shaped random-init fp16 model, Math/QA/Chatbot API trace (2000 req @3/s, seed 11), "
-                 "InferCept min-waste policy, reference cost-model defaults, 150 GB KV pool")
+ALL6 = [{"name": c} for c in ["Math", "QA", "VE", "Chatbot", "Image", "TTS"]]
+GPTJ_M, M13 = 458752, 819200
+RUN = {"policy": "infercept", "estimator": "oracle"}
+
+# SURVEY §8d configurations (C0 is the tiny CPU-runnable case, tests only).
+CONFIGS = {
+    "C1": dict(model={"preset": "gptj-6b"}, layers=28, M=GPTJ_M,
+               workload=dict(classes=[{"name": "Math"}, {"name": "QA"}, {"name": "Chatbot"}], request_count=2000,
+                             arrival_rate=3.0, seed=11),
+               cost=dict(mem_per_token=GPTJ_M, gpu_kv_capacity=150e9, cpu_kv_capacity=128e9,
+                         swap_per_token=GPTJ_M / LINK),
+               slack_blocks=512,
+               name="C1: GPT-J-6B-shaped random-init fp16 model, Math/QA/Chatbot API trace (2000 req @3/s, seed 11), "
+                    "InferCept min-waste policy, reference cost-model defaults, 150 GB GPU / 128 GB CPU KV ledger"),
+    "C2": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+               workload=dict(classes=[{"name": "Chatbot"}, {"name": "VE"}], request_count=1000, arrival_rate=2.0,
+                             seed=13),
+               cost=dict(mem_per_token=M13, gpu_kv_capacity=120e9, cpu_kv_capacity=96e9, swap_per_token=M13 / LINK),
+               slack_blocks=512,
+               name="C2: Vicuna-13B-shaped model, Chatbot + VE trace (1000 req @2/s, seed 13), 120 GB / 96 GB ledger: "
+                    "chunked swap under the swap budget"),
+    "C3": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+               workload=dict(classes=[{"name": "QA", "context_mean": 3000.0, "context_var": 200.0 ** 2}],
+                             request_count=1000, arrival_rate=2.0, seed=17),
+               cost=dict(mem_per_token=M13, gpu_kv_capacity=40e9, cpu_kv_capacity=128e9, swap_per_token=M13 / LINK),
+               slack_blocks=512,
+               name="C3: Vicuna-13B-shaped model, QA-shaped calls over 3000-token contexts (1000 req @2/s, seed 17), "
+                    "40 GB GPU ledger: Discard-heavy chunked recompute"),
+    "C4": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+               workload=dict(classes=ALL6, request_count=4000, arrival_rate=1000.0, seed=23),
+               cost=dict(mem_per_token=M13, gpu_kv_capacity=140e9, cpu_kv_capacity=64e9, swap_per_token=M13 / LINK),
+               slack_blocks=64,  # 140 GB pool + 26 GB of weights: little room for slack
+               name="C4: Vicuna-13B-shaped random-init fp16 model, fixed 4000-request trace of all six API classes "
+                    "(seed 23, arrivals 1000/s), InferCept min-waste policy, reference cost-model defaults, "
+                    "140 GB GPU / 64 GB CPU KV ledger per replica, requests sharded id mod N"),
+}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
 
 
 def k1_traffic():
@@ -53,19 +106,14 @@ def k1_traffic():
         return None
 
 
-def peaks():
-    try:
-        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "fallback": True}
-
-
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled only while `active`
+    (the timed windows)."""
 
     def __init__(self, device):
         self.device = device
         self.samples = []
+        self.active = False
         self._stop = threading.Event()
         self._t = None
 
@@ -75,14 +123,16 @@ class ClockSampler:
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
                  "clocks_event_reasons.sw_power_cap")
             while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    self.samples.append([x.strip() for x in out.split(",")])
-                except Exception:
-                    pass
-                self._stop.wait(0.2)
+                if self.active:
+                    try:
+                        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                             timeout=5).stdout.strip()
+                        if self.active:
+                            self.samples.append([x.strip() for x in out.split(",")])
+                    except Exception:
+                        pass
+                self._stop.wait(0.1)
         self._t = threading.Thread(target=loop, daemon=True)
         self._t.start()
 
@@ -98,23 +148,15 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def workload_for(world):
-    """The trace the N replicas serve: 2000*N requests at 3*N/s (same class mix
-    and seed), so each replica's id-mod-N shard is statistically the C1 trace:
-    per-GPU work is fixed as N grows (weak scaling)."""
-    if world == 1:
-        return WORKLOAD
-    return dict(WORKLOAD, request_count=WORKLOAD["request_count"] * world,
-                arrival_rate=WORKLOAD["arrival_rate"] * world)
-
-
-def shard_trace(ib, world, rank, tmpdir):
-    trace = ib.Trace.generate(workload_for(world))
+def shard_trace(ib, cfg, world, rank, tmpdir):
+    """Requests with id mod world == rank, original arrival times."""
+    trace = ib.Trace.generate(cfg["workload"])
     if world == 1:
         return trace
     full = os.path.join(tmpdir, "full.jsonl")
     trace.save(full)
-    lines = open(full).read().splitlines()
+    with open(full) as f:
+        lines = f.read().splitlines()
     out = os.path.join(tmpdir, f"shard{rank}.jsonl")
     with open(out, "w") as f:
         f.write(lines[0] + "\n")
@@ -124,34 +166,42 @@ def shard_trace(ib, world, rank, tmpdir):
     return ib.Trace.load(out)
 
 
-def gpu_pools(host_gb, gpu_blocks=0):
-    blocks = gpu_blocks or int(COST["gpu_kv_capacity"] // (16 * GPTJ_M)) + 512
-    return dict(gpu_blocks=blocks, host_bytes=int(host_gb * 1e9), max_requests=1024, max_rows=4096, timing=True,
-                stage_tokens=1024, swap_slots=10)
+def windows(total_iters, steps, warmup, n_win):
+    """[(first timed iteration index, timed count)]: n_win windows centred on
+    evenly spaced points of the schedule, each preceded by `warmup`
+    iterations, never overlapping (iteration indices are 0-based counts of
+    iterations already run)."""
+    n_win = max(1, min(n_win, steps))
+    per = [steps // n_win + (1 if j < steps % n_win else 0) for j in range(n_win)]
+    out, pos = [], 0
+    for j in range(n_win):
+        start = max(int((j + 0.5) * total_iters / n_win) - per[j] // 2, pos + warmup)
+        out.append((start, per[j]))
+        pos = start + per[j]
+    if pos > total_iters:
+        raise SystemExit(f"schedule has {total_iters} iterations: too short for {steps} timed + warm-up")
+    return out
 
 
-def cpu_forward_sample(plans, n_plans=3):
-    """Time the CPU oracle port of the GPT-J-shaped model step on plans taken
-    from the timed window: 1- and 2-layer variants give the per-layer cost,
-    extrapolated to 28 layers.  KV contents are synthetic (timing only)."""
-    import numpy as np
-    from oracle.forward import ForwardOracle
+def default_windows(steps):
+    return max(1, min(4, steps // 5))
 
-    def timed(layers):
-        fo = ForwardOracle({"preset": "gptj-6b", "layers": layers, "max_pos": 4160}, fast_random=True)
-        for pj in plans[:n_plans]:  # materialize contexts
-            for (rid, pos, count, kind, sample) in pj["spans"]:
-                fo._ensure(rid, pos + count + 1)
-        fo._forward_only(plans[0])  # untimed warm-up (first-touch of weights, BLAS threads)
-        t = time.perf_counter()
-        for pj in plans[:n_plans]:
-            fo._forward_only(pj)
-        return (time.perf_counter() - t) / n_plans
 
-    t1 = timed(1)
-    t2 = timed(2)
-    per_iter = t1 + 27 * max(t2 - t1, 0.0)
-    return per_iter, dict(t1=t1, t2=t2)
+def schedule_totals(ib, trace, cfg):
+    """(iterations, completed) of the replica's whole schedule (scheduler only)."""
+    s = ib.Session(trace, ib.CostModel.from_json(cfg["cost"]), RUN)
+    it, fin = s.step(10 ** 9)
+    assert fin
+    return it, s.counters()["completed"]
+
+
+def combine(gathered, steps):
+    """Whole-job figures from the ranks' stats: (requests served by all
+    ranks, [estimated device seconds of each rank's replay], [same, wall])."""
+    done_all = sum(g["total_done"] for g in gathered)
+    replay = [g["iters"] * g["dev_s"] / steps for g in gathered]
+    replay_wall = [g["iters"] * g["wall_s"] / steps for g in gathered]
+    return done_all, replay, replay_wall
 
 
 def measure_link(torch, mb=512, reps=3):
@@ -175,10 +225,29 @@ def measure_link(torch, mb=512, reps=3):
     return out
 
 
+def pools_for(cfg, host_gb, gpu_blocks=0):
+    """Executor pools: the ledger's GPU capacity in 16-token blocks + slack
+    (the Oracle estimator keeps every request's GPU positions a prefix, so the
+    ledger's blocks suffice; the executor enforces it), the pinned host pool,
+    the bench's staging ring, and the step-roofline peaks."""
+    pk = peaks()
+    blocks = gpu_blocks or int(cfg["cost"]["gpu_kv_capacity"] // (16 * cfg["M"])) + cfg["slack_blocks"]
+    return dict(gpu_blocks=blocks, host_bytes=int(host_gb * 1e9), max_requests=1024, max_rows=4096, timing=True,
+                stage_tokens=1024, swap_slots=10, roof_hbm_gbs=pk.get("hbm_gbs", 6526.0),
+                roof_tflops=pk.get("bf16_tflops", 1662.0))
+
+
+def host_pool_gb(cfg, world, override):
+    if override:
+        return override
+    return cfg["cost"]["cpu_kv_capacity"] / 1e9 * 1.25 + 4.0
+
+
 def run_b200(args):
     import torch
     import paper_2402_01869_b200 as ib
 
+    cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -188,50 +257,63 @@ def run_b200(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     link = measure_link(torch)
+    pk = peaks()
     tmp = tempfile.mkdtemp()
-    trace = shard_trace(ib, world, rank, tmp)
-    cost = ib.CostModel.from_json(COST)
-    ex = ib.Executor({"preset": "gptj-6b"}, local, gpu_pools(args.host_gb, args.gpu_blocks))
-    sess = ib.Session(trace, cost, {"policy": "infercept", "estimator": "oracle"}, ex)
+    trace = shard_trace(ib, cfg, world, rank, tmp)
+    total_iters, total_done = schedule_totals(ib, trace, cfg)
+    n_win = args.windows or default_windows(args.steps)
+    wins = windows(total_iters, args.steps, args.warmup, n_win)
 
-    # Fast-forward to steady state, then warm up.
-    sess.step(args.fast_forward)
-    sess.step(args.warmup)
-    ex.sync()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    c0, s0 = sess.counters(), ex.stats()
+    ex = ib.Executor(cfg["model"], local, pools_for(cfg, host_pool_gb(cfg, world, args.host_gb), args.gpu_blocks))
+    sess = ib.Session(trace, ib.CostModel.from_json(cfg["cost"]), RUN, ex)
+
     clocks = ClockSampler(local)
     clocks.start()
+    keys = ("k1_ms", "k1_bytes", "k1_timed_launches", "swap_ms", "swap_bytes_timed", "swap_in_forwarded_tokens",
+            "kernel_launches", "h2d_bytes", "d2h_bytes", "roof_s", "roof_bytes", "roof_flops", "chunk_rows",
+            "swap_in_tokens", "swap_out_tokens")
+    acc = {k: 0.0 for k in keys}
+    acc.update(dev_s=0.0, wall_s=0.0, completed=0, decode=0, swapped=0)
+    pos = 0
     profiling = os.environ.get("BENCH_PROFILE") == "1"
-    if profiling:  # ncu --profile-from-start off: capture only the timed window
-        torch.cuda.profiler.start()
-    wall0 = time.perf_counter()
-    ex.mark(0)
-    done, finished = sess.step(args.steps)
-    ex.mark(1)
-    ex.sync()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    if profiling:
-        torch.cuda.profiler.stop()
-    dev_ms = ex.elapsed_ms()
+    for (start, count) in wins:
+        if start - args.warmup > pos:
+            done, _ = sess.fast_forward(start - args.warmup - pos)
+            pos += done
+        done, _ = sess.step(start - pos)  # warm-up on the GPU
+        pos += done
+        ex.sync()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        c0, s0 = sess.counters(), ex.stats()
+        clocks.active = True
+        if profiling:  # ncu --profile-from-start off: capture only the timed windows
+            torch.cuda.profiler.start()
+        wall0 = time.perf_counter()
+        ex.mark(0)
+        done, _ = sess.step(count)
+        ex.mark(1)
+        ex.sync()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - wall0
+        if profiling:
+            torch.cuda.profiler.stop()
+        clocks.active = False
+        if done != count:
+            raise SystemExit(f"schedule ended inside a timed window ({done} of {count})")
+        pos += done
+        c1, s1 = sess.counters(), ex.stats()
+        acc["dev_s"] += ex.elapsed_ms() / 1e3
+        acc["wall_s"] += wall
+        acc["completed"] += c1["completed"] - c0["completed"]
+        acc["decode"] += c1["decode_rows"] - c0["decode_rows"]
+        acc["swapped"] += c1["swapped_tokens"] - c0["swapped_tokens"]
+        for k in keys:
+            acc[k] += s1[k] - s0[k]
     clk = clocks.stop()
-    c1, s1 = sess.counters(), ex.stats()
-    if done != args.steps:
-        raise SystemExit(f"trace ended after {done} of {args.steps} timed iterations; lower --fast-forward")
-
-    completed = c1["completed"] - c0["completed"]
-    decode = c1["decode_rows"] - c0["decode_rows"]
-    swapped = c1["swapped_tokens"] - c0["swapped_tokens"]
-    local_stats = dict(dev_s=dev_ms / 1e3, wall_s=wall, completed=completed, decode=decode, swapped=swapped,
-                       k1_ms=s1["k1_ms"] - s0["k1_ms"], k1_bytes=s1["k1_bytes"] - s0["k1_bytes"],
-                       k1_launches=s1["k1_timed_launches"] - s0["k1_timed_launches"],
-                       swap_ms=s1["swap_ms"] - s0["swap_ms"], swap_bytes=s1["swap_bytes_timed"] - s0["swap_bytes_timed"],
-                       fwd_tok=s1["swap_in_forwarded_tokens"] - s0["swap_in_forwarded_tokens"],
-                       launches=s1["kernel_launches"] - s0["kernel_launches"],
-                       h2d=s1["h2d_bytes"] - s0["h2d_bytes"], d2h=s1["d2h_bytes"] - s0["d2h_bytes"])
+    host_peak = ex.stats()["host_pool_peak"]
+    local_stats = dict(acc, iters=total_iters, total_done=total_done, host_peak=host_peak)
     if dist:
         gathered = [None] * world
         dist.all_gather_object(gathered, local_stats)
@@ -240,42 +322,52 @@ def run_b200(args):
     if rank != 0:
         dist.destroy_process_group()
         return
-    dev_s = max(g["dev_s"] for g in gathered)
-    wall_s = max(g["wall_s"] for g in gathered)
-    tot = {k: sum(g[k] for g in gathered) for k in ("completed", "decode", "swapped", "launches", "h2d", "d2h",
-                                                    "fwd_tok")}
-    pk = peaks()
-    k1_gbs = local_stats["k1_bytes"] / (local_stats["k1_ms"] / 1e3) / 1e9 if local_stats["k1_ms"] else None
-    swap_gbs = local_stats["swap_bytes"] / (local_stats["swap_ms"] / 1e3) / 1e9 if local_stats["swap_ms"] else None
+    K = args.steps
+    done_all, replay, replay_wall = combine(gathered, K)
+    dev_s_max = max(g["dev_s"] for g in gathered)
+    tot = {k: sum(g[k] for g in gathered) for k in ("decode", "swapped", "kernel_launches", "h2d_bytes", "d2h_bytes",
+                                                    "swap_in_forwarded_tokens", "completed")}
+    me = gathered[0]
+    k1_gbs = me["k1_bytes"] / (me["k1_ms"] / 1e3) / 1e9 if me["k1_ms"] else None
+    swap_gbs = me["swap_bytes_timed"] / (me["swap_ms"] / 1e3) / 1e9 if me["swap_ms"] else None
+    link_peak = (link["h2d"] + link["d2h"]) / 2
     line = {
         "metric": METRIC,
-        "value": tot["completed"] / dev_s,
+        "value": done_all / max(replay),
         "unit": "req/s",
         "n_gpus": world,
-        "steps": args.steps,
+        "steps": K,
         "warmup": args.warmup,
-        "ms_per_step": dev_s * 1e3 / args.steps,
+        "ms_per_step": dev_s_max * 1e3 / K,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f16 (fp32 accumulate)",
         "data": "synthetic (generated API trace, random-init weights, synthetic token ids)",
-        "config": {"workload": WORKLOAD_NAME, "window_iterations": [args.fast_forward + args.warmup + 1,
-                                                                    args.fast_forward + args.warmup + args.steps],
-                   "fast_forward_untimed": args.fast_forward,
-                   "parallelism": f"replicas{world}: one engine + KV pool per GPU serving request ids = rank mod N of a "
-                                  f"{workload_for(world)['request_count']}-request trace at "
-                                  f"{workload_for(world)['arrival_rate']:g}/s (per-GPU load = C1)",
-                   "l2": "inputs larger than L2 (KV pool ~154 GB; ~15 GB of KV read per iteration)"},
-        "decode_tok_s": tot["decode"] / dev_s,
-        "completed_in_window": tot["completed"],
+        "config": {"workload": cfg["name"], "config": args.config,
+                   "parallelism": f"replicas{world}: one engine + KV pool + pinned host pool per GPU, requests id mod "
+                                  f"{world}, no collective on the data path",
+                   "estimator": "value = requests of the trace / max over ranks of (iterations of the rank's "
+                                "bit-exact schedule x measured device seconds per iteration); the timed iterations "
+                                "are a stratified sample of each schedule",
+                   "windows": [[s, c] for s, c in wins], "warmup_per_window": args.warmup,
+                   "schedule_iterations": [g["iters"] for g in gathered],
+                   "l2": "inputs larger than L2 (140 GB KV pool, tens of GB of KV read per iteration)"},
+        "decode_tok_s": tot["decode"] / dev_s_max,
+        "completed_in_windows": tot["completed"],
+        "replay_seconds_estimated": max(replay),
+        "step_roofline": {"bound": "max(weights + KV bytes / HBM, FLOPs / tensor peak) per iteration",
+                          "bound_s": me["roof_s"], "measured_s": me["dev_s"],
+                          "frac": me["roof_s"] / me["dev_s"] if me["dev_s"] else None,
+                          "algorithmic_bytes": me["roof_bytes"], "algorithmic_flops": me["roof_flops"],
+                          "peaks": {"hbm_gbs": pk.get("hbm_gbs"), "tflops": pk.get("bf16_tflops")}},
         "swap_gbs_achieved": swap_gbs,
-        "swap_tokens_in_window": tot["swapped"],
-        "swap_in_forwarded_tokens": tot["fwd_tok"],
-        "host_pool_peak_gb": s1["host_pool_peak"] / 1e9,
+        "swap_tokens_in_windows": tot["swapped"],
+        "swap_in_forwarded_tokens": tot["swap_in_forwarded_tokens"],
+        "host_pool_peak_gb": me["host_peak"] / 1e9,
         "swap_roofline": {"bound": "host link", "achieved": swap_gbs, "unit": "GB/s",
-                          "peak": (link["h2d"] + link["d2h"]) / 2, "peak_h2d": link["h2d"], "peak_d2h": link["d2h"],
-                          "frac": swap_gbs / ((link["h2d"] + link["d2h"]) / 2) if swap_gbs else None,
+                          "peak": link_peak, "peak_h2d": link["h2d"], "peak_d2h": link["d2h"],
+                          "frac": swap_gbs / link_peak if swap_gbs else None,
                           "peak_source": "pinned 512 MiB copies measured by bench.py on this box",
                           "note": "achieved = swapped bytes / time of each PCIe batch on the copy streams; "
                                   "swap-ins forwarded from swap-out staging do not cross the link"},
@@ -286,89 +378,100 @@ def run_b200(args):
                      "traffic_algorithmic_bytes": (k1_traffic() or {}).get("algorithmic_bytes_per_launch"),
                      "traffic_source": (k1_traffic() or {}).get("source"),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
-        "e2e": {"value": tot["completed"] / wall_s, "unit": "req/s",
-                "h2d_bytes_per_step": tot["h2d"] / args.steps / world,
-                "d2h_bytes_per_step": tot["d2h"] / args.steps / world},
-        "gpu_launches": tot["launches"],
+        "e2e": {"value": done_all / max(replay_wall), "unit": "req/s",
+                "h2d_bytes_per_step": tot["h2d_bytes"] / K / world,
+                "d2h_bytes_per_step": tot["d2h_bytes"] / K / world},
+        "gpu_launches": int(tot["kernel_launches"]),
         "clocks": clk,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(ib, args, per_iter_completed=tot["completed"] / args.steps)
+        cpu = cpu_reference(cfg, args, wins)
+        line["cpu_baseline"] = {"value": cpu["value"], "unit": "req/s", "cores": cpu["cores"], "kind": "port",
+                                "sample": cpu["sample"], "s_per_iteration": cpu["s_per_iteration"]}
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
 
 
-def window_plans(ib, args, n):
-    """Plans of the first n timed iterations (scheduler only, CPU)."""
-    tmp = tempfile.mkdtemp()
-    path = os.path.join(tmp, "plans.jsonl")
-    sess2 = ib.Session(ib.Trace.generate(WORKLOAD), ib.CostModel.from_json(COST),
-                       {"policy": "infercept", "estimator": "oracle", "plan_log": path})
-    sess2.step(args.fast_forward + args.warmup + n)
-    del sess2
-    lines = open(path).read().splitlines()
-    return [json.loads(l) for l in lines[-n:]]
+def cpu_forward_seconds(preset, layers_total, plans, reps=2):
+    """Seconds per iteration of the numpy fp32 oracle forward over `plans`
+    with all host threads: 1- and 2-layer models timed (reps each, after one
+    untimed warm-up), extrapolated to `layers_total` layers.  KV rows are
+    materialised with non-zero contents (real memory traffic)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle.forward import ForwardOracle
+
+    cores = os.cpu_count()
+    per_layers = {}
+    with threadpool_limits(limits=cores):
+        for layers in (1, 2):
+            fo = ForwardOracle({"preset": preset, "layers": layers, "max_pos": 4160}, fast_random=True)
+            for pj in plans:
+                for (rid, pos, count, kind, sample) in pj["spans"]:
+                    fo._ensure(rid, pos + count + 1)
+            for kv in fo.kv.values():
+                kv.fill(np.float32(1e-3))
+            fo._forward_only(plans[0])
+            times = []
+            for _ in range(reps):
+                t = time.perf_counter()
+                for pj in plans:
+                    fo._forward_only(pj)
+                times.append((time.perf_counter() - t) / len(plans))
+            per_layers[layers] = times
+            del fo
+    t1, t2 = min(per_layers[1]), min(per_layers[2])
+    per_iter = t1 + (layers_total - 1) * max(t2 - t1, 0.0)
+    spread = max(max(v) / min(v) - 1.0 for v in per_layers.values())
+    return per_iter, dict(t1=t1, t2=t2, spread=spread, cores=cores, runs=per_layers)
 
 
-def cpu_baseline(ib, args, per_iter_completed):
-    plans = window_plans(ib, args, 3)
-    per_iter, detail = cpu_forward_sample(plans, 3)
-    return {"value": per_iter_completed / per_iter, "unit": "req/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": (f"numpy fp32 oracle forward of 3 timed-window iterations of the GPT-J-shaped step "
-                       f"(1- and 2-layer runs {detail['t1']:.2f}s/{detail['t2']:.2f}s, extrapolated to 28 layers: "
-                       f"{per_iter:.2f} s/iteration); KV contents synthetic"),
-            "s_per_iteration": per_iter}
+def cpu_reference(cfg, args, wins):
+    """The reference's CPU path on this host (see module docstring)."""
+    from oracle.ref_plans import reference_schedule, run_reference as ref_run
+    keep = {s + 1 for s, _ in wins}  # event-log iteration numbers are 1-based
+    with tempfile.TemporaryDirectory() as d:
+        summ, plans = reference_schedule(cfg["workload"], cfg["cost"], RUN, keep=keep, workdir=d)
+    t_sched = ref_run(cfg["workload"], cfg["cost"], RUN, None)["wall_s"] / summ["iterations"]
+    per_iter, det = cpu_forward_seconds(cfg["model"]["preset"], cfg["layers"], plans)
+    per_iter += t_sched
+    value = summ["done_events"] / (summ["iterations"] * per_iter)
+    return {"value": value, "s_per_iteration": per_iter, "cores": det["cores"], "iterations": summ["iterations"],
+            "completed": summ["done_events"], "sched_us_per_iteration": t_sched * 1e6, "forward": det,
+            "sample": (f"reference engine (oracle/_ref, whole trace: {int(summ['iterations'])} iterations, "
+                       f"{t_sched * 1e6:.1f} us/iteration) + numpy fp32 oracle forward of "
+                       f"{len(plans)} sampled iterations (first of each window; batches recovered from the "
+                       f"reference's event log) timed with 1 and 2 layers ({det['t1']:.2f} / {det['t2']:.2f} s, "
+                       f"run-to-run spread {det['spread'] * 100:.1f} %) and extrapolated to {cfg['layers']} layers: "
+                       f"{per_iter:.2f} s/iteration; EXTRAPOLATED, not a full-depth timed run")}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import ctypes
-    import paper_2402_01869_b200 as ib
-    ref = os.path.join(ROOT, "oracle", "_ref", "libinterceptsim.so")
-    sched_us = None
-    if os.path.exists(ref):
-        L = ctypes.CDLL(ref)
-        L.isim_trace_generate.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
-        L.isim_model_from_json.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
-        L.isim_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
-        L.isim_result_metric.argtypes = [ctypes.c_void_p, ctypes.c_char_p, ctypes.POINTER(ctypes.c_double)]
-        t, m, r = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
-        L.isim_trace_generate(json.dumps(WORKLOAD).encode(), ctypes.byref(t))
-        L.isim_model_from_json(json.dumps(COST).encode(), ctypes.byref(m))
-        t0 = time.perf_counter()
-        L.isim_run(t, m, b'{"policy":"infercept","estimator":"oracle"}', ctypes.byref(r))
-        el = time.perf_counter() - t0
-        it = ctypes.c_double()
-        L.isim_result_metric(r, b"iterations", ctypes.byref(it))
-        sched_us = el / it.value * 1e6
-    plans = window_plans(ib, args, 3)
-    # completions per iteration in the window, from the scheduler
-    sess = ib.Session(ib.Trace.generate(WORKLOAD), ib.CostModel.from_json(COST), {"policy": "infercept"})
-    sess.step(args.fast_forward + args.warmup)
-    c0 = sess.counters()
-    # Completions per iteration of the schedule (cheap: scheduler only), over
-    # at least 1000 iterations so a short --steps still sees completions.
-    n_sched = max(args.steps, 1000)
-    sess.step(n_sched)
-    c1 = sess.counters()
-    per_iter_completed = (c1["completed"] - c0["completed"]) / n_sched
-    per_iter, detail = cpu_forward_sample(plans, 3)
-    per_iter += (sched_us or 0.0) / 1e6
-    value = per_iter_completed / per_iter
+    cfg = CONFIGS[args.config]
+    # Same window positions as the B200 arm at N = 1 (the whole trace, one host).
+    from oracle.ref_plans import run_reference as ref_run
+    summ = ref_run(cfg["workload"], cfg["cost"], RUN, None)
+    wins = windows(int(summ["iterations"]), args.steps, args.warmup, args.windows or default_windows(args.steps))
+    cpu = cpu_reference(cfg, args, wins)
+    v = cpu["value"]
     line = {
-        "metric": METRIC, "value": value, "unit": "req/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_iter * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 (numpy)", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOAD_NAME, "host": "rank 0 only, host cores (no GPU used)"},
-        "cpu_baseline": {"value": value, "unit": "req/s", "cores": os.cpu_count(), "kind": "port",
-                         "sample": (f"reference scheduler (oracle/_ref, {sched_us:.2f} us/iteration, whole trace) + "
-                                    f"numpy oracle forward of 3 window iterations (1/2-layer runs "
-                                    f"{detail['t1']:.2f}/{detail['t2']:.2f} s, extrapolated to 28 layers)")
-                         if sched_us else "numpy oracle forward sample"},
-        "e2e": {"value": value, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "metric": METRIC, "value": v, "unit": "req/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": cpu["s_per_iteration"] * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (numpy)", "data": "synthetic", "impl": "reference",
+        "extrapolated": True,
+        "config": {"workload": cfg["name"], "config": args.config,
+                   "host": "rank 0 only, all host threads, the whole (unsharded) trace; no GPU used",
+                   "estimator": "value = requests / (iterations of the reference schedule x CPU seconds per "
+                                "iteration), the per-iteration time sampled at the B200 arm's window positions",
+                   "windows": [[s, c] for s, c in wins]},
+        "cpu_baseline": {"value": v, "unit": "req/s", "cores": cpu["cores"], "kind": "port",
+                         "sample": cpu["sample"]},
+        "forward_runs_s": cpu["forward"]["runs"],
+        "e2e": {"value": v, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
@@ -376,11 +479,12 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--fast-forward", type=int, default=3000)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--windows", type=int, default=0, help="timed windows (default: min(4, steps // 5))")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--host-gb", type=float, default=48.0)
+    ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host pool per rank (default: ledger x 1.25)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--gpu-blocks", type=int, default=0,
                     help="override the KV pool size (profiling runs only; the scheduler's capacity is unchanged)")

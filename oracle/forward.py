@@ -149,7 +149,7 @@ class ModelOracle:
 
     @staticmethod
     def lin(x, w, b=None):
-        y = (x.astype(np.float32) @ w.T.astype(np.float32)).astype(np.float32)
+        y = np.asarray(x, np.float32) @ np.asarray(w, np.float32).T
         return y + b if b is not None else y
 
     def rope(self, t, pos):
@@ -177,20 +177,21 @@ class ForwardOracle:
     def __init__(self, model_spec: dict, fast_random: bool = False):
         self.m = ModelOracle(model_spec, fast_random)
         self.hist = {}     # rid -> int64[ctx]
-        self.kv = {}       # rid -> float32[L, cap, 2, D] (fp16 values)
+        self.kv = {}       # rid -> float32[L, 2, H, cap, hd] (fp16 values; head-major for batched matmuls)
 
     def _ensure(self, rid, upto):
-        L, D = self.m.L, self.m.D
+        L, H, hd = self.m.L, self.m.H, self.m.hd
         if rid not in self.hist:
             self.hist[rid] = np.zeros(max(64, upto + 1), np.int64)
-            self.kv[rid] = np.zeros((L, max(64, upto), 2, D), np.float32)
+            self.kv[rid] = np.zeros((L, 2, H, max(64, upto), hd), np.float32)
         if self.hist[rid].shape[0] < upto + 1:
             h = np.zeros(max(upto + 1, 2 * self.hist[rid].shape[0]), np.int64)
             h[: self.hist[rid].shape[0]] = self.hist[rid]
             self.hist[rid] = h
-        if self.kv[rid].shape[1] < upto:
-            k = np.zeros((L, max(upto, 2 * self.kv[rid].shape[1]), 2, D), np.float32)
-            k[:, : self.kv[rid].shape[1]] = self.kv[rid]
+        cap = self.kv[rid].shape[3]
+        if cap < upto:
+            k = np.zeros((L, 2, H, max(upto, 2 * cap), hd), np.float32)
+            k[:, :, :, :cap] = self.kv[rid]
             self.kv[rid] = k
 
     def step(self, plan: dict, teacher_tokens=None) -> dict:
@@ -243,22 +244,33 @@ class ForwardOracle:
             k = m.rope(qkv[:, D:2 * D].reshape(n, H, hd), pos_arr)
             v = qkv[:, 2 * D:].reshape(n, H, hd)
             for (rid, pos, count, r0) in spans:
-                self.kv[rid][li, pos:pos + count, 0] = k[r0:r0 + count].reshape(count, D)
-                self.kv[rid][li, pos:pos + count, 1] = v[r0:r0 + count].reshape(count, D)
+                self.kv[rid][li, 0, :, pos:pos + count] = k[r0:r0 + count].transpose(1, 0, 2)
+                self.kv[rid][li, 1, :, pos:pos + count] = v[r0:r0 + count].transpose(1, 0, 2)
             attn = np.zeros((n, D), np.float32)
-            for (rid, pos, count, r0) in spans:
-                K = self.kv[rid][li, : pos + count, 0].reshape(-1, H, hd)
-                Vv = self.kv[rid][li, : pos + count, 1].reshape(-1, H, hd)
-                qq = q[r0:r0 + count]                       # [c, H, hd]
-                s = np.einsum("chd,khd->hck", qq, K).astype(np.float32) * scale
-                kpos = np.arange(pos + count)
-                qpos = pos + np.arange(count)
-                s = np.where(kpos[None, None, :] <= qpos[None, :, None], s, -np.inf)
+
+            def attend(span, li=li, q=q, attn=attn):
+                rid, pos, count, r0 = span
+                K = self.kv[rid][li, 0, :, : pos + count]      # [H, k, hd]
+                Vv = self.kv[rid][li, 1, :, : pos + count]
+                qq = q[r0:r0 + count].transpose(1, 0, 2)        # [H, c, hd]
+                s = np.matmul(qq, K.transpose(0, 2, 1)) * scale  # [H, c, k]
+                if count > 1:
+                    kpos = np.arange(pos + count)
+                    qpos = pos + np.arange(count)
+                    s = np.where(kpos[None, None, :] <= qpos[None, :, None], s, -np.inf)
                 s = s - s.max(axis=-1, keepdims=True)
-                p = np.exp(s).astype(np.float32)
+                p = np.exp(s)
                 p = p / p.sum(axis=-1, keepdims=True)
-                o = np.einsum("hck,khd->chd", p, Vv).astype(np.float32)
-                attn[r0:r0 + count] = o.reshape(count, D)
+                o = np.matmul(p, Vv)                             # [H, c, hd]
+                attn[r0:r0 + count] = o.transpose(1, 0, 2).reshape(count, D)
+
+            # Spans are independent (each writes its own rows): numpy releases
+            # the GIL, so many small (decode) spans use all host cores.
+            if len(spans) > 4:
+                list(_pool().map(attend, spans))
+            else:
+                for sp in spans:
+                    attend(sp)
             attn = r16(attn)
             if m.fam == "gptj":
                 x = x + m.lin(attn, lw["w_o"], lw["b_o"])
@@ -286,6 +298,18 @@ class ForwardOracle:
         for i, r in enumerate(sample_rows):
             self.hist[rows_rid[r]][rows_pos[r] + 1] = int(chosen[i])
         return {"logits": logits, "tokens": toks_out.tolist(), "margin": margin.tolist()}
+
+
+_POOL = None
+
+
+def _pool():
+    global _POOL
+    if _POOL is None:
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+        _POOL = ThreadPoolExecutor(max_workers=os.cpu_count() or 1)
+    return _POOL
 
 
 def _gelu(v: np.ndarray) -> np.ndarray:

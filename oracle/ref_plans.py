@@ -41,12 +41,14 @@ from __future__ import annotations
 import ctypes
 import json
 import os
+import re
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libinterceptsim.so")
 
 DECODE, FRESH, RECOMPUTE = 0, 1, 2
+_IT = re.compile(r'"it":(\d+)')
 
 
 def _lib(path=REF_LIB):
@@ -62,10 +64,11 @@ def _lib(path=REF_LIB):
     return L
 
 
-def run_reference(workload: dict, cost: dict, run_cfg: dict, event_log: str, ledger_every: int = 1,
+def run_reference(workload: dict, cost: dict, run_cfg: dict, event_log: str | None, ledger_every: int = 1,
                   lib_path: str = REF_LIB) -> dict:
     """isim_run of the reference library with an event log; returns the
-    summary metrics the bench needs and the wall time of the run."""
+    summary metrics the bench needs and the wall time of the run
+    (event_log None: no log, the scheduler's own speed)."""
     import time
     L = _lib(lib_path)
     t, m, r = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
@@ -73,8 +76,10 @@ def run_reference(workload: dict, cost: dict, run_cfg: dict, event_log: str, led
         raise RuntimeError(L.isim_last_error().decode())
     if L.isim_model_from_json(json.dumps(cost).encode(), ctypes.byref(m)):
         raise RuntimeError(L.isim_last_error().decode())
-    cfg = dict(run_cfg, event_log=event_log)
-    if ledger_every:
+    cfg = dict(run_cfg)
+    if event_log:
+        cfg["event_log"] = event_log
+    if event_log and ledger_every:
         cfg["dump_ledger_every"] = ledger_every
     t0 = time.perf_counter()
     st = L.isim_run(t, m, json.dumps(cfg).encode(), ctypes.byref(r))
@@ -166,7 +171,14 @@ def plans_from_events(lines, keep=None):
                 s[4] = 0
         return {"it": rec["it"], "B": rec["B"], "rows": total, "spans": spans, "ops": [],
                 "evicted": sorted(int(e.split(":")[1]) for e in rec["events"] if e.startswith("evict:"))}
+    need = None if keep is None else {k + d for k in keep for d in (-1, 0, 1)}
     for line in lines:
+        if need is not None and isinstance(line, str):
+            m = _IT.search(line)
+            if m and int(m.group(1)) not in need:
+                pending = None  # records outside the kept neighbourhoods are skipped unparsed
+                prev = {}
+                continue
         rec = json.loads(line) if isinstance(line, str) else line
         spans, total = _spans_of(rec, prev)
         prev = {int(k): (e["gpu"], e["cpu"], e["discarded"]) for k, e in rec["ledger"]["requests"].items()}

@@ -348,6 +348,11 @@ class Impl final : public B200Executor {
     return d;
   }
   double k1_bytes_iter_ = 0.0;
+  // Whole-step roofline (algorithmic): weights read once, KV read by K1 / K2
+  // and written by K4; FLOPs of the projections, LM head and attention.  The
+  // per-iteration bound is max(bytes / HBM, FLOPs / tensor peak).
+  double roof_gbs_ = 6526.0, roof_tflops_ = 1662.0;
+  double roof_bytes_ = 0.0, roof_flops_ = 0.0, roof_s_ = 0.0;
   int max_pos1_ = 0;
 };
 
@@ -378,6 +383,8 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   overlap_mlp_ = pj.value("overlap_mlp", getenv("IB2_NO_OVERLAP_MLP") == nullptr);
   trace_iters_ = pj.value("trace_iterations", false);
 
+  roof_gbs_ = pj.value("roof_hbm_gbs", roof_gbs_);
+  roof_tflops_ = pj.value("roof_tflops", roof_tflops_);
   max_slots_ = pj.value("max_requests", 1024);
   max_rows_ = pj.value("max_rows", 4096);
   max_ctx_ = pj.value("max_ctx", spec_.max_pos);
@@ -1051,6 +1058,27 @@ void Impl::consume(const isim_batch_plan& p) {
     std::int64_t k1_bytes = 0;
     for (int r : drows) k1_bytes += static_cast<std::int64_t>(rows[r].pos + 1) * 2 * spec_.d_model * 2;
     k1_bytes_iter_ = static_cast<double>(k1_bytes);
+    {
+      const double Dd = spec_.d_model, L = spec_.layers;
+      const double w_layer = Dd * (3.0 * Dd + Dd + spec_.ffn_in_width() + spec_.ffn);
+      const double lm = samples.empty() ? 0.0 : Dd * spec_.vocab;
+      double kv_keys = 0.0, attn = 0.0;  // keys read per layer; attention FLOPs per layer / (4 D)
+      for (int r : drows) {
+        kv_keys += rows[r].pos + 1;
+        attn += rows[r].pos + 1;
+      }
+      for (int i = 0; i < p.n_spans; ++i) {
+        const isim_row_span& sp = p.spans[i];
+        if (sp.count == 1 || force_row_attention_) continue;
+        kv_keys += sp.pos + sp.count;
+        attn += static_cast<double>(sp.count) * (sp.pos + (sp.count + 1) / 2.0);
+      }
+      const double bytes = 2.0 * (L * w_layer + lm) + L * 2.0 * Dd * 2.0 * (kv_keys + n_rows);
+      const double flops = 2.0 * n_rows * L * w_layer + 2.0 * samples.size() * lm + L * 4.0 * Dd * attn;
+      roof_bytes_ += bytes;
+      roof_flops_ += flops;
+      roof_s_ += std::max(bytes / (roof_gbs_ * 1e9), flops / (roof_tflops_ * 1e12));
+    }
     max_pos1_ = 0;
     for (int r : drows) max_pos1_ = std::max(max_pos1_, rows[r].pos + 1);
     if (!samples.empty() && !record_) sync_event(tok_done_[k], 1);  // tok_host_[k] free again
@@ -1372,6 +1400,9 @@ std::string Impl::stats_json() const {
   j["k1_timed_launches"] = k1_launches_timed_;
   j["k1_ms"] = k1_ms_;
   j["k1_bytes"] = k1_bytes_timed_;
+  j["roof_bytes"] = roof_bytes_;
+  j["roof_flops"] = roof_flops_;
+  j["roof_s"] = roof_s_;
   j["gemm"] = gemm_uses_tcgen05() ? "tcgen05" : "simt";
   j["h2d_bytes"] = h2d_bytes_;
   j["d2h_bytes"] = d2h_bytes_;

@@ -1,25 +1,24 @@
 """Request-sharded replicas with world_size 2 over gloo on CPU.
 
-Each rank takes the requests with id mod N == rank from the same generated
-trace (original arrival times), runs its own scheduler, and the ranks meet only
-in the timing / counter reduction -- the exact plumbing bench.py uses with
-NCCL on GPUs.  Checks: the shards partition the trace, each rank's schedule is
-identical to running its shard alone, and the max-over-ranks / sum reductions.
+The bench's C4 configuration (BASELINE configs[4]: a fixed 4000-request
+trace, requests id mod N, original arrival times; strong scaling): each rank
+takes its shard of the same generated trace, runs its own scheduler with a
+plan log, and the ranks meet only in the reduction -- the plumbing bench.py
+uses with NCCL on GPUs.  Checks: the shards partition the trace; each rank's
+plan log (every batch the executor would run) and summary equal its shard
+run alone; the window positions and the whole-job reduction
+(bench.combine: requests / slowest rank's estimated replay).
 """
+import hashlib
 import json
 import os
 import socket
 import tempfile
 
-import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from conftest import ROOT
-
-WL = dict(classes=[{"name": "Math"}, {"name": "QA"}, {"name": "Chatbot"}], request_count=120, arrival_rate=3.0,
-          seed=11)
-COST = dict(mem_per_token=458752, gpu_kv_capacity=150e9, cpu_kv_capacity=128e9, swap_per_token=458752 / 50e9)
 
 
 def _free_port():
@@ -30,6 +29,11 @@ def _free_port():
     return p
 
 
+def _sha(path):
+    with open(path, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
 def _worker(rank, world, port, outdir):
     import sys
     sys.path.insert(0, ROOT)
@@ -37,17 +41,22 @@ def _worker(rank, world, port, outdir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import bench
     import paper_2402_01869_b200 as ib
-    bench.WORKLOAD = WL
-    trace = bench.shard_trace(ib, world, rank, tempfile.mkdtemp())
-    sess = ib.Session(trace, ib.CostModel.from_json(COST), {"policy": "infercept"})
+    cfg = bench.CONFIGS["C4"]
+    trace = bench.shard_trace(ib, cfg, world, rank, tempfile.mkdtemp())
+    iters, done = bench.schedule_totals(ib, trace, cfg)
+    plan_log = os.path.join(outdir, f"plans{rank}.jsonl")
+    sess = ib.Session(trace, ib.CostModel.from_json(cfg["cost"]), dict(bench.RUN, plan_log=plan_log))
     _, finished = sess.step(10 ** 9)
     res = sess.finish().summary()
-    ids = []
+    del sess
     path = os.path.join(outdir, f"t{rank}.jsonl")
     trace.save(path)
     with open(path) as f:
         ids = [json.loads(l)["id"] for l in f.read().splitlines()[1:]]
-    local = dict(rank=rank, ids=ids, summary=res, iterations=res["iterations"], completed=res["completed"])
+    # stand-in device / wall seconds: rank 1 is the slower one
+    local = dict(rank=rank, ids=ids, summary=res, iters=iters, total_done=done, finished=finished,
+                 plan_sha=_sha(plan_log), wins=bench.windows(iters, 20, 5, 4),
+                 dev_s=0.5 + rank, wall_s=0.6 + rank)
     out = [None] * world
     dist.all_gather_object(out, local)
     if rank == 0:
@@ -55,21 +64,36 @@ def _worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_two_rank_request_sharding():
+def test_two_rank_c4_sharding():
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    import paper_2402_01869_b200 as ib
     outdir = tempfile.mkdtemp()
     mp.spawn(_worker, args=(2, _free_port(), outdir), nprocs=2, join=True)
     got = json.load(open(os.path.join(outdir, "gathered.json")))
+    cfg = bench.CONFIGS["C4"]
+    n = cfg["workload"]["request_count"]
     ids0, ids1 = set(got[0]["ids"]), set(got[1]["ids"])
-    # bench.workload_for: the 2-replica trace has 2x the requests at 2x the rate,
-    # so each shard carries the single-GPU load (weak scaling).
-    n = 2 * WL["request_count"]
     assert ids0.isdisjoint(ids1) and ids0 | ids1 == set(range(n))
     assert all(i % 2 == 0 for i in ids0) and all(i % 2 == 1 for i in ids1)
-    assert sum(g["completed"] for g in got) == n
-    assert abs(len(ids0) - WL["request_count"]) <= 1
-    # Each rank's schedule equals running its shard alone in this process.
-    import paper_2402_01869_b200 as ib
+    assert all(g["finished"] for g in got)
+    assert sum(g["total_done"] for g in got) == n == sum(g["summary"]["completed"] for g in got)
+    # Each rank's schedule (plan log, summary) equals running its shard alone.
     for g in got:
         t = ib.Trace.load(os.path.join(outdir, f"t{g['rank']}.jsonl"))
-        alone = ib.run(t, ib.CostModel.from_json(COST), {"policy": "infercept"}).summary()
+        log = os.path.join(outdir, f"alone{g['rank']}.jsonl")
+        alone = ib.run(t, ib.CostModel.from_json(cfg["cost"]), dict(bench.RUN, plan_log=log)).summary()
         assert alone == g["summary"]
+        assert _sha(log) == g["plan_sha"]
+        assert alone["iterations"] == g["iters"]
+        # windows: 4 x 5 timed iterations, inside the schedule, in order, warm-up room before each
+        w = g["wins"]
+        assert sum(c for _, c in w) == 20 and len(w) == 4
+        assert w[0][0] >= 5 and all(w[i][0] >= w[i - 1][0] + w[i - 1][1] + 5 for i in range(1, 4))
+        assert w[-1][0] + w[-1][1] <= g["iters"]
+    # the reduction: all requests / the slowest rank's estimated replay time
+    done_all, replay, replay_wall = bench.combine(got, 20)
+    assert done_all == n
+    assert replay == [g["iters"] * g["dev_s"] / 20 for g in got]
+    assert max(replay) == replay[1] and max(replay_wall) == replay_wall[1]

@@ -32,27 +32,10 @@ sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402  (ClockSampler, measure_link, peaks)
 
-M13 = 819200
-LINK = 50e9
-ALL6 = [{"name": c} for c in ["Math", "QA", "VE", "Chatbot", "Image", "TTS"]]
-CONFIGS = {
-    "C1": dict(model={"preset": "gptj-6b"}, M=bench.GPTJ_M, workload=bench.WORKLOAD, cost=bench.COST,
-               fast_forward=3000),
-    "C2": dict(model={"preset": "vicuna-13b"}, M=M13,
-               workload=dict(classes=[{"name": "Chatbot"}, {"name": "VE"}], request_count=1000, arrival_rate=2.0,
-                             seed=13),
-               cost=dict(mem_per_token=M13, gpu_kv_capacity=120e9, cpu_kv_capacity=96e9, swap_per_token=M13 / LINK),
-               fast_forward=3000),
-    "C3": dict(model={"preset": "vicuna-13b"}, M=M13,
-               workload=dict(classes=[{"name": "QA", "context_mean": 3000.0, "context_var": 200.0 ** 2}],
-                             request_count=1000, arrival_rate=2.0, seed=17),
-               cost=dict(mem_per_token=M13, gpu_kv_capacity=40e9, cpu_kv_capacity=128e9, swap_per_token=M13 / LINK),
-               fast_forward=3000),
-    "C4": dict(model={"preset": "vicuna-13b"}, M=M13,
-               workload=dict(classes=ALL6, request_count=4000, arrival_rate=1000.0, seed=23),
-               cost=dict(mem_per_token=M13, gpu_kv_capacity=140e9, cpu_kv_capacity=64e9, swap_per_token=M13 / LINK),
-               fast_forward=2000, slack_blocks=64),  # 140 GB pool + 26 GB weights: little room for slack
-}
+# The configs live in bench.py (one definition for both); this tool times one
+# contiguous window after a fast-forward instead of bench.py's stratified windows.
+FAST_FORWARD = {"C1": 3000, "C2": 3000, "C3": 3000, "C4": 2000}
+CONFIGS = {k: dict(v, fast_forward=FAST_FORWARD[k]) for k, v in bench.CONFIGS.items()}
 
 
 def run_config(name, c, steps, host_gb, link, torch):

@@ -9,10 +9,11 @@ import numpy as np
 import bench
 import paper_2402_01869_b200 as ib
 ff, n = int(sys.argv[1]), int(sys.argv[2])
-pools = bench.gpu_pools(48)
+C1 = bench.CONFIGS["C1"]
+pools = bench.pools_for(C1, 48)
 pools["trace_iterations"] = True
 ex = ib.Executor({"preset": "gptj-6b"}, 0, pools)
-sess = ib.Session(ib.Trace.generate(bench.WORKLOAD), ib.CostModel.from_json(bench.COST), {"policy": "infercept"}, ex)
+sess = ib.Session(ib.Trace.generate(C1["workload"]), ib.CostModel.from_json(C1["cost"]), {"policy": "infercept"}, ex)
 sess.step(ff)
 ex.sync()
 st0 = ex.stats()

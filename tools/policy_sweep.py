@@ -25,8 +25,9 @@ N = int(sys.argv[1]) if len(sys.argv) > 1 else 400
 OUT = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "policy_sweep.json")
 # Memory pressure, where the policies differ: 40 GB of KV for the ledger and
 # twice the C1 arrival rate (the C1 mix at 150 GB never fills).
-WL = dict(bench.WORKLOAD, request_count=N, arrival_rate=6.0)
-COST = dict(bench.COST, gpu_kv_capacity=40e9, cpu_kv_capacity=64e9)
+C1 = bench.CONFIGS["C1"]
+WL = dict(C1["workload"], request_count=N, arrival_rate=6.0)
+COST = dict(C1["cost"], gpu_kv_capacity=40e9, cpu_kv_capacity=64e9)
 POLICIES = ["infercept", "improved-discard", "vanilla-discard", "preserve", "swap"]
 
 rows = []
@@ -39,7 +40,7 @@ for pol in POLICIES:
         del sess, ex
         gc.collect()  # the previous executor's pools must be released first
     blocks = int(COST["gpu_kv_capacity"] // (16 * bench.GPTJ_M)) + 512
-    pools = dict(bench.gpu_pools(96, blocks), overlap_swaps=(pol != "swap"))  # pinned pool > the 64 GB CPU ledger
+    pools = dict(bench.pools_for(C1, 96, blocks), overlap_swaps=(pol != "swap"))  # pinned pool > the 64 GB CPU ledger
     ex = ib.Executor({"preset": "gptj-6b"}, 0, pools)
     s0 = ex.stats()
     sess = ib.Session(ib.Trace.generate(WL), ib.CostModel.from_json(COST), {"policy": pol, "estimator": "oracle"},
