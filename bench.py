@@ -406,7 +406,8 @@ def cpu_forward_seconds(preset, layers_total, plans, reps=2):
     per_layers = {}
     with threadpool_limits(limits=cores):
         for layers in (1, 2):
-            fo = ForwardOracle({"preset": preset, "layers": layers, "max_pos": 4160}, fast_random=True)
+            fo = ForwardOracle({"preset": preset, "layers": layers, "max_pos": 4160}, fast_random=True,
+                               precision="f32")
             for pj in plans:
                 for (rid, pos, count, kind, sample) in pj["spans"]:
                     fo._ensure(rid, pos + count + 1)

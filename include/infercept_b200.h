@@ -165,6 +165,10 @@ isim_status isim_exec_free_blocks(const isim_exec* ex, int64_t* out);
 /* Raw KV bytes of [pos_lo,pos_hi) of one request, layer-major, for swap checks. */
 isim_status isim_exec_read_kv(const isim_exec* ex, int64_t request_id, int64_t pos_lo, int64_t pos_hi, void* out,
                               int64_t capacity);
+/* Token ids of positions [pos_lo,pos_hi) of a request's device token history
+ * (synthetic prompt / API-returned ids and sampled ids). */
+isim_status isim_exec_read_history(const isim_exec* ex, int64_t request_id, int64_t pos_lo, int64_t pos_hi,
+                                   int32_t* out, int64_t capacity);
 /* Device timing on the executor's compute stream: op 0 marks the start, op 1
  * the stop; op 2 waits for the stop mark and writes the elapsed ms. */
 isim_status isim_exec_timer(isim_exec* ex, int32_t op, double* out_ms);

@@ -7,9 +7,15 @@ Parity status: *unpinned* for model arithmetic.  The reference (interceptsim)
 has no model -- its model step is the analytic CostModel::t_fwd
 (proj/include/interceptsim/cost_model.hpp:33-37, called at
 proj/src/engine.cpp:460) -- so there are no logits or token ids to pin against.
-This module restates the forward the executor runs, in float32 numpy with the
-same fp16 rounding points (GEMM inputs, q/k/v, attention output, KV cache), and
-consumes the very BatchPlans the scheduler emits.  The *scheduling* that
+This module restates the forward the executor runs with the same fp16
+rounding points (GEMM inputs, q/k/v, attention output, KV cache, fp32
+residual stream), and consumes the very BatchPlans the scheduler emits.
+Between rounding points it accumulates in float64 by default (the parity
+reference: the exact value each fp16 rounding point rounds; two fp32
+implementations with different summation orders land on different sides of
+an fp16 rounding boundary about twice as often as either does against the
+exact value), or in float32 (precision="f32": the bench's CPU timing sample,
+a plain fp32 CPU implementation).  The *scheduling* that
 produces those plans is pinned bit-exactly against the reference itself
 (oracle/_ref, see tests/test_sched_parity.py).
 
@@ -40,13 +46,29 @@ def mix64(z: np.ndarray) -> np.ndarray:
 
 
 def synth_weight(seed: int, tensor_id: int, count: int) -> np.ndarray:
-    """Device init kernel restated: exec/common.cuh synth_weight."""
+    """Device init kernel restated: exec/common.cuh synth_weight (element-wise,
+    so large tensors are hashed in pieces on the thread pool)."""
     with np.errstate(over="ignore"):
         base = mix64(np.uint64((seed + 0x9E3779B97F4A7C15 * (tensor_id + 1)) & 0xFFFFFFFFFFFFFFFF))
-        h = mix64(base + np.arange(count, dtype=np.uint64))
-    u24 = (h >> np.uint64(40)).astype(np.float32)
-    u = u24 * np.float32(1.1920928955078125e-07) - np.float32(1.0)
-    return u * np.float32(0.034641016)
+    out = np.empty(count, np.float32)
+
+    def piece(lo, hi=None):
+        hi = min(count, lo + _PIECE)
+        with np.errstate(over="ignore"):
+            h = mix64(base + np.arange(lo, hi, dtype=np.uint64))
+        u24 = (h >> np.uint64(40)).astype(np.float32)
+        out[lo:hi] = (u24 * np.float32(1.1920928955078125e-07) - np.float32(1.0)) * np.float32(0.034641016)
+
+    starts = range(0, count, _PIECE)
+    if count > _PIECE:
+        list(_pool().map(piece, starts))
+    else:
+        for lo in starts:
+            piece(lo)
+    return out
+
+
+_PIECE = 1 << 22
 
 
 def synth_token(seed: int, rid: int, pos, vocab: int):
@@ -56,9 +78,10 @@ def synth_token(seed: int, rid: int, pos, vocab: int):
 
 
 def r16(x: np.ndarray) -> np.ndarray:
-    """Round float32 to IEEE fp16 (nearest-even), returned as float32: the
-    executor's storage type for weights, activations and the KV cache."""
-    return np.asarray(x, dtype=np.float32).astype(np.float16).astype(np.float32)
+    """Round to IEEE fp16 (nearest-even; float64 inputs round directly, no
+    double rounding), returned as float32: the executor's storage type for
+    weights, activations and the KV cache."""
+    return np.asarray(x).astype(np.float16).astype(np.float32)
 
 
 PRESETS = {
@@ -71,10 +94,12 @@ PRESETS = {
 class ModelOracle:
     """Weights + forward of one model (exec/model.cpp layout_weights order)."""
 
-    def __init__(self, spec: dict, fast_random: bool = False):
+    def __init__(self, spec: dict, fast_random: bool = False, precision: str = "f64"):
         # fast_random: plain numpy normals instead of the device hash, for the
         # bench's CPU timing sample only (values then differ from the device).
+        # precision: accumulation type between the fp16 rounding points.
         self.fast_random = fast_random
+        self.A = {"f64": np.float64, "f32": np.float32}[precision]
         s = dict(PRESETS[spec.get("preset", "tiny")])
         s.update({k: v for k, v in spec.items() if k != "preset"})
         s.setdefault("max_pos", 4160)
@@ -125,31 +150,34 @@ class ModelOracle:
         tid = self._next_id
         self._next_id += 1
         if kind == 1:
-            return np.ones(count, np.float32)
+            return np.ones(count, self.A)
         if kind == 2:
-            return np.zeros(count, np.float32)
+            return np.zeros(count, self.A)
         if self.fast_random:
-            return (np.random.default_rng(tid).standard_normal(count, dtype=np.float32) * np.float32(0.02))
-        return r16(synth_weight(self.s["weight_seed"], tid, count))
+            w = np.random.default_rng(tid).standard_normal(count, dtype=np.float32) * np.float32(0.02)
+        else:
+            w = r16(synth_weight(self.s["weight_seed"], tid, count))
+        return w if self.A is np.float32 else w.astype(self.A)
 
     # ---- pieces ---------------------------------------------------------------
     def norm(self, x, g, b):
-        x = x.astype(np.float32)
+        A = self.A
+        x = np.asarray(x, A)
+        eps = A(np.float32(self.s["norm_eps"]))
         if self.fam == "llama":
-            var = np.mean(x * x, axis=-1, keepdims=True, dtype=np.float32)
-            y = x * (np.float32(1.0) / np.sqrt(var + np.float32(self.s["norm_eps"]))) * g
+            var = np.mean(x * x, axis=-1, keepdims=True, dtype=A)
+            y = x * (A(1.0) / np.sqrt(var + eps)) * g
         else:
-            mu = np.mean(x, axis=-1, keepdims=True, dtype=np.float32)
+            mu = np.mean(x, axis=-1, keepdims=True, dtype=A)
             d = x - mu
-            var = np.mean(d * d, axis=-1, keepdims=True, dtype=np.float32)
-            y = d * (np.float32(1.0) / np.sqrt(var + np.float32(self.s["norm_eps"]))) * g
+            var = np.mean(d * d, axis=-1, keepdims=True, dtype=A)
+            y = d * (A(1.0) / np.sqrt(var + eps)) * g
             if b is not None:
                 y = y + b
-        return r16(y.astype(np.float32))
+        return r16(y)
 
-    @staticmethod
-    def lin(x, w, b=None):
-        y = np.asarray(x, np.float32) @ np.asarray(w, np.float32).T
+    def lin(self, x, w, b=None):
+        y = np.asarray(x, self.A) @ w.T
         return y + b if b is not None else y
 
     def rope(self, t, pos):
@@ -157,9 +185,9 @@ class ModelOracle:
         if not self.rot:
             return t
         half = self.rot // 2
-        c = self.cos[pos][:, None, :]
-        s = self.sin[pos][:, None, :]
-        t = t.copy()
+        c = self.cos[pos][:, None, :].astype(self.A)
+        s = self.sin[pos][:, None, :].astype(self.A)
+        t = t.astype(self.A)
         if self.fam == "gptj":
             a, b = t[..., 0:self.rot:2].copy(), t[..., 1:self.rot:2].copy()
             t[..., 0:self.rot:2] = a * c - b * s
@@ -174,8 +202,8 @@ class ModelOracle:
 class ForwardOracle:
     """Replays BatchPlans (dicts from the scheduler's plan log) on the CPU."""
 
-    def __init__(self, model_spec: dict, fast_random: bool = False):
-        self.m = ModelOracle(model_spec, fast_random)
+    def __init__(self, model_spec: dict, fast_random: bool = False, precision: str = "f64"):
+        self.m = ModelOracle(model_spec, fast_random, precision)
         self.hist = {}     # rid -> int64[ctx]
         self.kv = {}       # rid -> float32[L, 2, H, cap, hd] (fp16 values; head-major for batched matmuls)
 
@@ -183,14 +211,14 @@ class ForwardOracle:
         L, H, hd = self.m.L, self.m.H, self.m.hd
         if rid not in self.hist:
             self.hist[rid] = np.zeros(max(64, upto + 1), np.int64)
-            self.kv[rid] = np.zeros((L, 2, H, max(64, upto), hd), np.float32)
+            self.kv[rid] = np.zeros((L, 2, H, max(64, upto), hd), self.m.A)
         if self.hist[rid].shape[0] < upto + 1:
             h = np.zeros(max(upto + 1, 2 * self.hist[rid].shape[0]), np.int64)
             h[: self.hist[rid].shape[0]] = self.hist[rid]
             self.hist[rid] = h
         cap = self.kv[rid].shape[3]
         if cap < upto:
-            k = np.zeros((L, 2, H, max(upto, 2 * cap), hd), np.float32)
+            k = np.zeros((L, 2, H, max(upto, 2 * cap), hd), self.m.A)
             k[:, :, :, :cap] = self.kv[rid]
             self.kv[rid] = k
 
@@ -235,8 +263,9 @@ class ForwardOracle:
         toks = np.array([self.hist[r][p] for r, p in zip(rows_rid, rows_pos)])
         x = m.tok_emb[toks].astype(np.float32)
         if m.pos_emb is not None:
-            x = x + m.pos_emb[pos_arr]
-        scale = np.float32(1.0 / math.sqrt(hd))
+            x = (x + m.pos_emb[pos_arr]).astype(np.float32)
+        A = m.A
+        scale = A(np.float32(1.0 / math.sqrt(hd)))
         for li, lw in enumerate(m.layers):
             xn = m.norm(x, lw["ln1_g"], lw["ln1_b"])
             qkv = r16(m.lin(xn, lw["w_qkv"], lw["b_qkv"]))
@@ -272,21 +301,22 @@ class ForwardOracle:
                 for sp in spans:
                     attend(sp)
             attn = r16(attn)
+            # x is the executor's fp32 residual stream: rounded to fp32 after every add.
             if m.fam == "gptj":
-                x = x + m.lin(attn, lw["w_o"], lw["b_o"])
+                x = (x + m.lin(attn, lw["w_o"], lw["b_o"])).astype(np.float32)
                 u = m.lin(xn, lw["w_in"], lw["b_in"])
                 u = r16(_gelu(u))
-                x = x + m.lin(u, lw["w_out"], lw["b_out"])
+                x = (x + m.lin(u, lw["w_out"], lw["b_out"])).astype(np.float32)
             else:
-                x = x + m.lin(attn, lw["w_o"], lw["b_o"])
+                x = (x + m.lin(attn, lw["w_o"], lw["b_o"])).astype(np.float32)
                 xn2 = m.norm(x, lw["ln2_g"], lw["ln2_b"])
                 if m.fam == "llama":
                     gu = m.lin(xn2, lw["w_in"])
                     g, u = gu[:, 0::2], gu[:, 1::2]
-                    h = r16((g / (np.float32(1) + np.exp(-g))) * u)
+                    h = r16((g / (A(1) + np.exp(-g))) * u)
                 else:
                     h = r16(_gelu(m.lin(xn2, lw["w_in"], lw["b_in"])))
-                x = x + m.lin(h, lw["w_out"], lw["b_out"])
+                x = (x + m.lin(h, lw["w_out"], lw["b_out"])).astype(np.float32)
         if not sample_rows:
             return {"logits": np.zeros((0, V), np.float32), "tokens": [], "margin": []}
         xs = m.norm(x[sample_rows], m.lnf_g, m.lnf_b)
@@ -313,6 +343,6 @@ def _pool():
 
 
 def _gelu(v: np.ndarray) -> np.ndarray:
-    v = v.astype(np.float32)
-    return (np.float32(0.5) * v * (np.float32(1.0) + np.tanh(np.float32(0.7978845608028654) *
-                                                           (v + np.float32(0.044715) * v * v * v)))).astype(np.float32)
+    A = v.dtype.type
+    c0, c1 = A(np.float32(0.7978845608028654)), A(np.float32(0.044715))
+    return A(0.5) * v * (A(1.0) + np.tanh(c0 * (v + c1 * v * v * v)))

@@ -246,6 +246,12 @@ class Executor(_Handle):
         _abi.check(_L.isim_exec_read_kv(self._ptr, request_id, lo, hi, out.ctypes.data, out.nbytes))
         return out
 
+    def read_history(self, request_id: int, lo: int, hi: int):
+        import numpy as np
+        out = np.empty(hi - lo, dtype=np.int32)
+        _abi.check(_L.isim_exec_read_history(self._ptr, request_id, lo, hi, out.ctypes.data, out.size))
+        return out
+
 
 class Session(_Handle):
     """isim_session_*: the scheduler stepped K iterations at a time."""

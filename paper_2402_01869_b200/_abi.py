@@ -49,7 +49,7 @@ EXPORTS = [
     "isim_run", "isim_result_summary_json", "isim_result_write_requests_csv", "isim_result_metric",
     "isim_result_free",
     "isim_exec_create", "isim_exec_step", "isim_exec_sync", "isim_exec_stats_json", "isim_exec_last_tokens",
-    "isim_exec_last_logits", "isim_exec_block_table", "isim_exec_free_blocks", "isim_exec_read_kv", "isim_exec_timer", "isim_exec_free",
+    "isim_exec_last_logits", "isim_exec_block_table", "isim_exec_free_blocks", "isim_exec_read_kv", "isim_exec_read_history", "isim_exec_timer", "isim_exec_free",
     "isim_session_open", "isim_session_step", "isim_session_fast_forward", "isim_session_counters", "isim_session_finish", "isim_session_free",
     "isim_debug_gemm", "isim_debug_tile_weights",
 ]
@@ -96,6 +96,7 @@ def _load():
         "isim_exec_block_table": (ctypes.c_int, [V, I64, ctypes.POINTER(I32), I32, ctypes.POINTER(I32)]),
         "isim_exec_free_blocks": (ctypes.c_int, [V, ctypes.POINTER(I64)]),
         "isim_exec_read_kv": (ctypes.c_int, [V, I64, I64, I64, V, I64]),
+        "isim_exec_read_history": (ctypes.c_int, [V, I64, I64, I64, V, I64]),
         "isim_exec_timer": (ctypes.c_int, [V, I32, ctypes.POINTER(D)]),
         "isim_exec_free": (None, [V]),
         "isim_session_open": (ctypes.c_int, [V, V, S, V, P]),

@@ -120,6 +120,8 @@ class Impl final : public B200Executor {
   std::int32_t block_table(std::int64_t request_id, std::int32_t* out, std::int32_t cap) const override;
   std::int64_t free_blocks() const override;
   void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out, std::int64_t cap) const override;
+  void read_history(std::int64_t request_id, std::int64_t lo, std::int64_t hi, std::int32_t* out,
+                    std::int64_t cap) const override;
   bool measure_steps() override {
     step_clock_ = true;
     return true;
@@ -1449,6 +1451,18 @@ std::int64_t Impl::free_blocks() const {
   std::int32_t t = 0;
   IB2_CUDA(cudaMemcpy(&t, top_, 4, cudaMemcpyDeviceToHost));
   return t;
+}
+
+void Impl::read_history(std::int64_t rid, std::int64_t lo, std::int64_t hi, std::int32_t* out,
+                        std::int64_t cap) const {
+  auto it = slot_of_.find(rid);
+  if (it == slot_of_.end()) throw DeviceError("read_history: unknown request");
+  if (lo < 0 || hi < lo || hi > hist_stride_) throw DeviceError("read_history: positions out of range");
+  if (cap < hi - lo) throw DeviceError("read_history: buffer too small");
+  IB2_CUDA(cudaStreamSynchronize(main_));
+  if (hi > lo)
+    IB2_CUDA(cudaMemcpy(out, hist_ + static_cast<std::int64_t>(it->second) * hist_stride_ + lo, (hi - lo) * 4,
+                        cudaMemcpyDeviceToHost));
 }
 
 void Impl::read_kv(std::int64_t rid, std::int64_t lo, std::int64_t hi, void* out, std::int64_t cap) const {

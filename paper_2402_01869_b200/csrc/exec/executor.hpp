@@ -33,6 +33,10 @@ class B200Executor : public PlanSink {
   virtual double timer(int op) = 0;
   virtual void read_kv(std::int64_t request_id, std::int64_t lo, std::int64_t hi, void* out,
                        std::int64_t cap) const = 0;
+  // Token ids of positions [lo,hi) of a request's device history (synthetic
+  // prompt / API-returned ids and sampled ids, as the embed kernel reads them).
+  virtual void read_history(std::int64_t request_id, std::int64_t lo, std::int64_t hi, std::int32_t* out,
+                            std::int64_t cap) const = 0;
 };
 
 // Kernel test hook behind isim_debug_gemm (exec/k_gemm_tc.cu).

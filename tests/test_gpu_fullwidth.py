@@ -1,0 +1,76 @@
+"""Full-width numeric parity on the real configurations' schedules.
+
+The bench configs' models at their real width -- GPT-J-6B (d 4096, 16 heads
+of 256, ffn 16384, vocab 50400) and Vicuna-13B (d 5120, 40 heads of 128,
+SwiGLU ffn 13824, vocab 32000) -- cut to 2 layers, replaying what the
+scheduler actually emitted for C1 / C2 / C3.  A request's rows
+attend only over its own context, so the plan log restricted to a few
+requests (their spans and KV ops, every iteration they appear in) is itself a
+valid plan sequence: the executor runs exactly the batches those requests saw
+in the full schedule -- prompt chunks, decode rows over 1-3k contexts,
+swap-outs and swap-ins under the budget, discards and ~2k-row recompute
+chunks -- and oracle/forward.py replays the same plans.  Checked as in
+test_gpu_model.replay: logits of every sampled row within 1e-3 relative,
+greedy ids equal except flagged near-ties, block tables / free-list size bit
+exact, swapped KV bytes bit exact after the round trip.
+"""
+import json
+
+import pytest
+
+from conftest import have_gpu
+from test_gpu_model import pools_for, replay
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs a B200")]
+
+# Requests picked from each schedule for what they exercise (scheduler-only
+# survey of the plan logs): rows = iterations with rows for the request.
+CASES = {
+    # C1: swap-out + swap-in, a discard and a 463-row recompute (662); a
+    # 1001-row recompute chunk (707)
+    "C1": dict(model={"preset": "gptj-6b", "layers": 2}, rids=[662, 707]),
+    # C2: swaps + 914-row recompute (571); 2,531-token context, 2,043-row recompute (992)
+    "C2": dict(model={"preset": "vicuna-13b", "layers": 2}, rids=[571, 992]),
+    # C3: ~3k-token context, swaps, 2,031-row recompute chunk (300)
+    "C3": dict(model={"preset": "vicuna-13b", "layers": 2}, rids=[300]),
+}
+
+
+def filtered_plans(name, rids, tmp_path):
+    import bench
+    import paper_2402_01869_b200 as ib
+    cfg = bench.CONFIGS[name]
+    path = str(tmp_path / f"{name}.jsonl")
+    ib.run(ib.Trace.generate(cfg["workload"]), ib.CostModel.from_json(cfg["cost"]), dict(bench.RUN, plan_log=path))
+    keep = set(rids)
+    out = []
+    with open(path) as f:
+        for line in f:
+            p = json.loads(line)
+            spans = [s for s in p["spans"] if s[0] in keep]
+            ops = [o for o in p["ops"] if o[0] in keep]
+            if spans or ops:
+                out.append(dict(p, spans=spans, ops=ops, B=sum(s[2] for s in spans)))
+    return out, cfg
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_fullwidth_parity_on_config_schedule(tmp_path, name):
+    import paper_2402_01869_b200 as ib
+    case = CASES[name]
+    plans, cfg = filtered_plans(name, case["rids"], tmp_path)
+    kinds = {o[1] for p in plans for o in p["ops"]}
+    assert {ib.KV_SWAP_OUT, ib.KV_SWAP_IN, ib.KV_RELEASE} <= kinds
+    rec = max((s[2] for p in plans for s in p["spans"] if s[3] == ib.SPAN_RECOMPUTE), default=0)
+    ctx = max(s[1] + s[2] for p in plans for s in p["spans"])
+    preset = case["model"]["preset"]
+    d = {"gptj-6b": 4096, "vicuna-13b": 5120}[preset]
+    model_m = 2 * 2 * d * 2  # KV bytes per token of the 2-layer model
+    pools = pools_for(dict(cfg["cost"], gpu_kv_capacity=8 * 4160 * cfg["M"], cpu_kv_capacity=8 * 4160 * cfg["M"]),
+                      model_m, max_requests=16, max_rows=4096)
+    r = replay(plans, case["model"], pools, len(plans), check_tables_every=1)
+    assert r["sampled"] > 50
+    assert r["ties"] <= max(2, r["sampled"] // 200)
+    assert r["kv_checked"] > 0, "no swapped bytes were round-tripped"
+    print(name, preset, f"{len(plans)} iterations, max recompute chunk {rec}, max context {ctx}",
+          {k: v for k, v in r.items() if k != "stats"})
