@@ -32,7 +32,9 @@ def pools_for(cost, model_m, **kw):
     return d
 
 
-def replay(plans, model, pools, n_iters, check_tables_every=1, kv_check=True):
+def replay(plans, model, pools, n_iters, check_tables_every=1, kv_check=True, errors=None, rtol=LOGIT_RTOL):
+    """errors: optional list collecting (iteration, span, kind, count, pos,
+    rel err) of every sampled row."""
     import paper_2402_01869_b200 as ib
     from oracle.blocktable import BlockTableOracle
     from oracle.forward import ForwardOracle
@@ -61,11 +63,15 @@ def replay(plans, model, pools, n_iters, check_tables_every=1, kv_check=True):
         ref = fo.step(plan_j, teacher_tokens=dev_tok)
         if dev_tok:
             glog = ex.last_logits().reshape(len(dev_tok), -1)
+            sampled_spans = [s for s in plan_j["spans"] if s[4]]
             for i, t in enumerate(dev_tok):
                 scale = float(np.max(np.abs(ref["logits"][i])))
                 err = float(np.max(np.abs(glog[i] - ref["logits"][i]))) / scale
                 worst = max(worst, err)
-                assert err <= LOGIT_RTOL, f"iteration {plan_j['it']} row {i}: logits rel err {err:.2e}"
+                if errors is not None:
+                    sp = sampled_spans[i]
+                    errors.append((plan_j["it"], sp[0], sp[3], sp[2], sp[1], err))
+                assert err <= rtol, f"iteration {plan_j['it']} row {i}: logits rel err {err:.2e}"
                 if t != ref["tokens"][i]:
                     assert ref["margin"][i] <= TIE_FRAC * scale, (plan_j["it"], i, t, ref["tokens"][i], ref["margin"][i])
                     ties += 1
