@@ -189,6 +189,8 @@ class Impl final : public B200Executor {
   bool record_ = false, timing_ = false;
   bool force_row_attention_ = false;  // diagnostics: every row through K1
   bool fused_qkv_ = false;            // K4 in the QKV GEMM epilogue (opt-in)
+  bool split_batch_ = true;           // decode / chunk rows as two micro-batches on two streams
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   // diagnostics: per-iteration start events on the compute stream + the
   // iteration's composition (rows, decode rows, chunk rows, swap-in, swap-out)
   bool trace_iters_ = false;
@@ -374,6 +376,8 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   IB2_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
   IB2_CUDA(cudaStreamCreateWithFlags(&copy_in_, cudaStreamNonBlocking));
   IB2_CUDA(cudaStreamCreateWithFlags(&aux_, cudaStreamNonBlocking));
+  IB2_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  IB2_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   for (int i = 0; i < kSeqRing; ++i) {
     IB2_CUDA(cudaEventCreateWithFlags(&d2h_ring_[i], cudaEventDisableTiming));
     IB2_CUDA(cudaEventCreateWithFlags(&h2d_ring_[i], cudaEventDisableTiming));
@@ -383,6 +387,7 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   force_row_attention_ = pj.value("row_attention", false);
   fused_qkv_ = pj.value("fused_qkv", getenv("IB2_FUSED_QKV") != nullptr);
   overlap_mlp_ = pj.value("overlap_mlp", getenv("IB2_NO_OVERLAP_MLP") == nullptr);
+  split_batch_ = pj.value("split_batch", getenv("IB2_NO_SPLIT_BATCH") == nullptr);
   trace_iters_ = pj.value("trace_iterations", false);
 
   roof_gbs_ = pj.value("roof_hbm_gbs", roof_gbs_);
@@ -578,6 +583,8 @@ Impl::~Impl() {
   cudaStreamDestroy(copy_);
   cudaStreamDestroy(copy_in_);
   cudaStreamDestroy(aux_);
+  cudaEventDestroy(ev_fork_);
+  cudaEventDestroy(ev_join_);
   for (cudaEvent_t e : ev_ln_) cudaEventDestroy(e);
   for (cudaEvent_t e : ev_mlp_) cudaEventDestroy(e);
   if (mlp_) cudaFree(mlp_);
@@ -951,21 +958,31 @@ void Impl::consume(const isim_batch_plan& p) {
   std::vector<RowDesc> rows;
   std::vector<std::int32_t> drows, samples;
   std::vector<TileDesc> tiles;
-  for (int i = 0; i < p.n_spans; ++i) {
-    const isim_row_span& sp = p.spans[i];
-    const int slot = slot_for(sp.request_id);
-    const int r0 = static_cast<int>(rows.size());
-    if (sp.pos + sp.count > max_ctx_) throw DeviceError("executor: row position beyond max_ctx");
-    for (int k = 0; k < sp.count; ++k)
-      rows.push_back({slot, sp.pos + k, sp.kind == ISIM_SPAN_FRESH ? 1 : 0, 0, sp.request_id});
-    if (sp.count == 1 || force_row_attention_) {
-      for (int k = 0; k < sp.count; ++k) drows.push_back(r0 + k);
-    } else {
-      for (int k = 0; k < sp.count; k += kChunkTileRows)
-        tiles.push_back({r0 + k, std::min(kChunkTileRows, sp.count - k), slot, sp.pos + k, 0, 0, -1, 0});
+  // Rows of single-row spans (K1) first, then the chunk spans' rows (K2): the
+  // two groups are the forward's micro-batches (split_batch_).  Sampling rows
+  // stay in span order.
+  std::vector<int> span_r0(p.n_spans);
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int i = 0; i < p.n_spans; ++i) {
+      const isim_row_span& sp = p.spans[i];
+      const bool single = sp.count == 1 || force_row_attention_;
+      if (single != (pass == 0)) continue;
+      const int slot = slot_for(sp.request_id);
+      const int r0 = static_cast<int>(rows.size());
+      span_r0[i] = r0;
+      if (sp.pos + sp.count > max_ctx_) throw DeviceError("executor: row position beyond max_ctx");
+      for (int k = 0; k < sp.count; ++k)
+        rows.push_back({slot, sp.pos + k, sp.kind == ISIM_SPAN_FRESH ? 1 : 0, 0, sp.request_id});
+      if (single) {
+        for (int k = 0; k < sp.count; ++k) drows.push_back(r0 + k);
+      } else {
+        for (int k = 0; k < sp.count; k += kChunkTileRows)
+          tiles.push_back({r0 + k, std::min(kChunkTileRows, sp.count - k), slot, sp.pos + k, 0, 0, -1, 0});
+      }
     }
-    if (sp.sample) samples.push_back(r0 + sp.count - 1);
   }
+  for (int i = 0; i < p.n_spans; ++i)
+    if (p.spans[i].sample) samples.push_back(span_r0[i] + p.spans[i].count - 1);
   const int n_rows = static_cast<int>(rows.size());
   if (n_rows > max_rows_) throw DeviceError("executor: batch exceeds max_rows");
   if (static_cast<int>(samples.size()) > max_samples_ || static_cast<int>(drows.size()) > max_samples_)
@@ -1171,98 +1188,134 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
   const int D = m.d_model, F = m.ffn;
   const KvGeom g = geom();
   const bool rms = m.family == Family::Llama;
-  auto gemm_on = [&](cudaStream_t st, const f16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias, f16* out,
-                     int ldo, float* outf, int ldf, int M, const float* addf) {
+  // Micro-batches (split_batch_): the decode rows [0, n_drows) and the chunk
+  // rows [n_drows, n) are independent (different requests), so each runs its
+  // own layer chain on its own stream -- the decode chain (weight-streaming
+  // GEMMs + K1: HBM bound) on aux_, the chunk chain (tensor-core GEMMs + K2)
+  // on main_ -- and the GPU overlaps HBM-bound with tensor-bound work.  The
+  // weights are read once per chain.
+  const bool split = split_batch_ && n_drows > 0 && n_drows < n && !force_row_attention_;
+  auto gemm_on = [&](cudaStream_t st, int off, const f16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias,
+                     f16* out, int ldo, float* outf, int ldf, int M, const float* addf) {
     GemmArgs ga{a, weights_ + w, M, N, K, epi, W(bias), out, ldo, outf, ldf};
     ga.addf = addf;
+    ga.a_rows = max_rows_ - off;  // TMA bounds of an A operand that starts at row `off`
     launch_gemm(ga, st);
     ++kernel_launches_;
   };
-  auto gemm = [&](const f16* a, std::int64_t w, int N, int K, Epi epi, std::int64_t bias, f16* out, int ldo,
-                  float* outf, int ldf, int M) { gemm_on(main_, a, w, N, K, epi, bias, out, ldo, outf, ldf, M, nullptr); };
-  const bool overlap = overlap_mlp_ && m.parallel_residual();
+  const bool overlap = !split && overlap_mlp_ && m.parallel_residual();
   // Interleaved (GPT-J) or no rotary: RoPE pairs are adjacent columns, so the
   // QKV GEMM epilogue can apply it and write K/V into the pool itself.
   // Opt-in (IB2_FUSED_QKV=1): measured 2.5 % slower end to end than the
   // separate K4 pass on C1 -- the epilogue's dependent row/table loads sit on
   // the QKV GEMM's critical path (one tile per CTA), costing more than K4.
-  const bool fused_qkv = fused_qkv_ && (m.rotary_dim == 0 || m.family == Family::GptJ) && D % 64 == 0;
+  const bool fused_qkv = !split && fused_qkv_ && (m.rotary_dim == 0 || m.family == Family::GptJ) && D % 64 == 0;
   launch_embed(rows_dev_, n, hist_, hist_stride_, W(wl_.tok_emb), W(wl_.pos_emb), D, m.token_seed, m.vocab, x_, main_);
   ++kernel_launches_;
+  if (split) {
+    IB2_CUDA(cudaEventRecord(ev_fork_, main_));
+    IB2_CUDA(cudaStreamWaitEvent(aux_, ev_fork_, 0));
+  }
   const int timed_layer = m.layers / 2;
-  for (int l = 0; l < m.layers; ++l) {
+  // One layer over rows [off, off + cnt) on stream st.  attn: 1 = K1 only
+  // (decode chain), 2 = K2 only (chunk chain), 3 = both (unsplit batch).
+  auto layer_rows = [&](cudaStream_t st, int off, int cnt, int attn, int l) {
     const LayerWeights& lw = wl_.layer[l];
-    launch_norm(x_, D, nullptr, n, D, W(lw.ln1_g), W(lw.ln1_b), rms, m.norm_eps, xn_, D, main_);
+    float* x = x_ + static_cast<std::int64_t>(off) * D;
+    f16* xn = xn_ + static_cast<std::int64_t>(off) * D;
+    f16* qkv = qkv_ + static_cast<std::int64_t>(off) * 3 * D;
+    f16* at = attn_ + static_cast<std::int64_t>(off) * D;
+    f16* hid = hid_ + static_cast<std::int64_t>(off) * F;
+    const bool dec = (attn & 1) && n_drows > 0;
+    launch_norm(x, D, nullptr, cnt, D, W(lw.ln1_g), W(lw.ln1_b), rms, m.norm_eps, xn, D, st);
+    ++kernel_launches_;
     // The layer whose K1 is timed for the roofline keeps its MLP branch inline,
-    // so K1's events measure it without concurrent kernels.
-    const bool overlap_l = overlap && !(timing_ && l == timed_layer && n_drows > 0);
+    // so K1's events measure it without concurrent kernels of this chain.
+    const bool overlap_l = overlap && !(timing_ && l == timed_layer && dec);
     if (overlap_l) {  // MLP branch on aux_: fc_in(ln1(x)) -> GELU -> fc_out -> mlp_ (fp32, + bias)
-      IB2_CUDA(cudaEventRecord(ev_ln_[l], main_));
+      IB2_CUDA(cudaEventRecord(ev_ln_[l], st));
       IB2_CUDA(cudaStreamWaitEvent(aux_, ev_ln_[l], 0));
-      gemm_on(aux_, xn_, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid_, F, nullptr, 0, n, nullptr);
-      gemm_on(aux_, hid_, lw.w_out, D, F, Epi::StoreF32, lw.b_out, nullptr, 0, mlp_, D, n, nullptr);
+      gemm_on(aux_, off, xn, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid, F, nullptr, 0, cnt, nullptr);
+      gemm_on(aux_, off, hid, lw.w_out, D, F, Epi::StoreF32, lw.b_out, nullptr, 0, mlp_, D, cnt, nullptr);
       IB2_CUDA(cudaEventRecord(ev_mlp_[l], aux_));
     }
     if (fused_qkv) {
       // K4 fused into the QKV epilogue: q (RoPE) -> qkv_, k (RoPE) / v -> pool.
-      GemmArgs ga{xn_, weights_ + lw.w_qkv, n, 3 * D, D, Epi::QkvRopeKv, W(lw.b_qkv), qkv_, 3 * D, nullptr, 0,
+      GemmArgs ga{xn, weights_ + lw.w_qkv, cnt, 3 * D, D, Epi::QkvRopeKv, W(lw.b_qkv), qkv, 3 * D, nullptr, 0,
                   QkvWrite{rows_dev_, g.pool, l * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks,
                            m.heads, m.head_dim(), m.rotary_dim, rope_cs_}};
-      launch_gemm(ga, main_);
+      launch_gemm(ga, st);
       ++kernel_launches_;
     } else {
-      gemm(xn_, lw.w_qkv, 3 * D, D, Epi::StoreF16, lw.b_qkv, qkv_, 3 * D, nullptr, 0, n);
-      launch_rope_kv_write(qkv_, rows_dev_, n, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, main_);
+      gemm_on(st, off, xn, lw.w_qkv, 3 * D, D, Epi::StoreF16, lw.b_qkv, qkv, 3 * D, nullptr, 0, cnt, nullptr);
+      launch_rope_kv_write(qkv, rows_dev_ + off, cnt, g, l, m.rotary_dim, m.family == Family::GptJ, rope_cs_, st);
       kernel_launches_ += 2;
     }
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    const bool time_k1 = timing_ && l == timed_layer && n_drows > 0;
-    if (time_k1) {
-      if (ev_free_.empty()) {
-        cudaEvent_t a, b;
-        IB2_CUDA(cudaEventCreate(&a));
-        IB2_CUDA(cudaEventCreate(&b));
-        ev_free_.push_back({a, b});
+    if (attn & 1) {
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      const bool time_k1 = timing_ && l == timed_layer && n_drows > 0;
+      if (time_k1) {
+        if (ev_free_.empty()) {
+          cudaEvent_t a, b;
+          IB2_CUDA(cudaEventCreate(&a));
+          IB2_CUDA(cudaEventCreate(&b));
+          ev_free_.push_back({a, b});
+        }
+        e0 = ev_free_.back().first;
+        e1 = ev_free_.back().second;
+        ev_free_.pop_back();
+        IB2_CUDA(cudaEventRecord(e0, st));
       }
-      e0 = ev_free_.back().first;
-      e1 = ev_free_.back().second;
-      ev_free_.pop_back();
-      IB2_CUDA(cudaEventRecord(e0, main_));
+      launch_decode_attention(qkv_, drows_dev_, rows_dev_, n_drows, g, l, max_pos1_, part_o_, part_ml_, attn_,
+                              k1_counters_, st);
+      if (n_drows) ++kernel_launches_;
+      if (time_k1) {
+        IB2_CUDA(cudaEventRecord(e1, st));
+        ev_pending_.push_back({e0, e1});
+        ev_bytes_.push_back(k1_bytes_iter_ + static_cast<double>(n_drows) * 2.0 * D * 2);
+      }
     }
-    launch_decode_attention(qkv_, drows_dev_, rows_dev_, n_drows, g, l, max_pos1_, part_o_, part_ml_, attn_,
-                              k1_counters_, main_);
-    if (n_drows) ++kernel_launches_;
-    if (time_k1) {
-      IB2_CUDA(cudaEventRecord(e1, main_));
-      ev_pending_.push_back({e0, e1});
-      ev_bytes_.push_back(k1_bytes_iter_ + static_cast<double>(n_drows) * 2.0 * D * 2);
+    if (attn & 2) {
+      launch_chunk_attention(qkv_, max_rows_, tiles_dev_, n_tiles, combines_dev_, n_combines_, g, l, attn_,
+                             chunk_ws_o_, chunk_ws_ml_, st);
+      if (n_tiles) kernel_launches_ += n_combines_ > 0 ? 2 : 1;
     }
-    launch_chunk_attention(qkv_, max_rows_, tiles_dev_, n_tiles, combines_dev_, n_combines_, g, l, attn_,
-                           chunk_ws_o_, chunk_ws_ml_, main_);
-    if (n_tiles) kernel_launches_ += n_combines_ > 0 ? 2 : 1;
     if (overlap_l) {
       // x = (x + attn W_o) + mlp: the MLP branch ran on aux_.
-      IB2_CUDA(cudaStreamWaitEvent(main_, ev_mlp_[l], 0));
-      gemm_on(main_, attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n, mlp_);
+      IB2_CUDA(cudaStreamWaitEvent(st, ev_mlp_[l], 0));
+      gemm_on(st, off, at, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x, D, cnt, mlp_);
     } else if (m.parallel_residual()) {
       // GPT-J: x += attn W_o + mlp(ln1(x)); both read the same xn.
-      gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
-      gemm(xn_, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid_, F, nullptr, 0, n);
-      gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
+      gemm_on(st, off, at, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x, D, cnt, nullptr);
+      gemm_on(st, off, xn, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid, F, nullptr, 0, cnt, nullptr);
+      gemm_on(st, off, hid, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x, D, cnt, nullptr);
     } else {
-      gemm(attn_, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x_, D, n);
-      launch_norm(x_, D, nullptr, n, D, W(lw.ln2_g), W(lw.ln2_b), rms, m.norm_eps, xn_, D, main_);
+      gemm_on(st, off, at, lw.w_o, D, D, Epi::ResidAdd, lw.b_o, nullptr, 0, x, D, cnt, nullptr);
+      launch_norm(x, D, nullptr, cnt, D, W(lw.ln2_g), W(lw.ln2_b), rms, m.norm_eps, xn, D, st);
       ++kernel_launches_;
       if (m.family == Family::Llama)
-        gemm(xn_, lw.w_in, 2 * F, D, Epi::SwiGluF16, -1, hid_, F, nullptr, 0, n);
+        gemm_on(st, off, xn, lw.w_in, 2 * F, D, Epi::SwiGluF16, -1, hid, F, nullptr, 0, cnt, nullptr);
       else
-        gemm(xn_, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid_, F, nullptr, 0, n);
-      gemm(hid_, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x_, D, n);
+        gemm_on(st, off, xn, lw.w_in, F, D, Epi::GeluF16, lw.b_in, hid, F, nullptr, 0, cnt, nullptr);
+      gemm_on(st, off, hid, lw.w_out, D, F, Epi::ResidAdd, lw.b_out, nullptr, 0, x, D, cnt, nullptr);
     }
+  };
+  for (int l = 0; l < m.layers; ++l) {
+    if (split) {
+      layer_rows(aux_, 0, n_drows, 1, l);
+      layer_rows(main_, n_drows, n - n_drows, 2, l);
+    } else {
+      layer_rows(main_, 0, n, 3, l);
+    }
+  }
+  if (split) {
+    IB2_CUDA(cudaEventRecord(ev_join_, aux_));
+    IB2_CUDA(cudaStreamWaitEvent(main_, ev_join_, 0));
   }
   if (n_samples > 0) {
     launch_norm(x_, D, samples_dev_, n_samples, D, W(wl_.lnf_g), W(wl_.lnf_b), rms, m.norm_eps, lmrows_, D, main_);
-    gemm(lmrows_, wl_.lm_w, m.vocab, D, Epi::StoreF32, wl_.lm_b, nullptr, 0, logits_, m.vocab, n_samples);
+    gemm_on(main_, 0, lmrows_, wl_.lm_w, m.vocab, D, Epi::StoreF32, wl_.lm_b, nullptr, 0, logits_, m.vocab,
+            n_samples, nullptr);
     launch_argmax(logits_, n_samples, m.vocab, samples_dev_, rows_dev_, hist_, hist_stride_, out_tok_, tok_out_host_,
                   main_);
     kernel_launches_ += 2;

@@ -765,7 +765,7 @@ void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
     IB2_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
     configured = true;
   }
-  const std::int64_t a_rows = g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M;
+  const std::int64_t a_rows = a.a_rows > 0 ? a.a_rows : (g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, 128);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, 128);
   const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
@@ -895,10 +895,10 @@ void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
       GemmArgs c = a;
       c.M = std::min(128, a.M - m0);
       c.a = a.a + static_cast<std::int64_t>(m0) * a.K;
+      c.a_rows = (a.a_rows > 0 ? a.a_rows : cap) - m0;
       if (c.out) c.out = a.out + static_cast<std::int64_t>(m0) * a.ldo;
       if (c.outf) c.outf = a.outf + static_cast<std::int64_t>(m0) * a.ldf;
       if (c.addf) c.addf = a.addf + static_cast<std::int64_t>(m0) * a.ldf;
-      c.a_rows = cap - m0;
       launch_skinny<128, 5>(c, s);
     }
   } else {
