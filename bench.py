@@ -238,9 +238,19 @@ def pools_for(cfg, host_gb, gpu_blocks=0):
 
 
 def host_pool_gb(cfg, world, override):
+    """Pinned host pool per rank: the CPU ledger x 1.25 (extent rounding and
+    staging) + 4 GB, capped at 3/4 of the host's available memory shared by
+    the ranks on this node."""
     if override:
         return override
-    return cfg["cost"]["cpu_kv_capacity"] / 1e9 * 1.25 + 4.0
+    want = cfg["cost"]["cpu_kv_capacity"] / 1e9 * 1.25 + 4.0
+    try:
+        with open("/proc/meminfo") as f:
+            avail = next(int(l.split()[1]) for l in f if l.startswith("MemAvailable")) * 1024 / 1e9
+        local = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+        return min(want, 0.75 * avail / max(1, local))
+    except Exception:
+        return want
 
 
 def run_b200(args):

@@ -189,7 +189,7 @@ class Impl final : public B200Executor {
   bool record_ = false, timing_ = false;
   bool force_row_attention_ = false;  // diagnostics: every row through K1
   bool fused_qkv_ = false;            // K4 in the QKV GEMM epilogue (opt-in)
-  bool split_batch_ = true;           // decode / chunk rows as two micro-batches on two streams
+  bool split_batch_ = false;          // decode / chunk rows as two micro-batches on two streams (opt-in)
   cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   // diagnostics: per-iteration start events on the compute stream + the
   // iteration's composition (rows, decode rows, chunk rows, swap-in, swap-out)
@@ -387,7 +387,10 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   force_row_attention_ = pj.value("row_attention", false);
   fused_qkv_ = pj.value("fused_qkv", getenv("IB2_FUSED_QKV") != nullptr);
   overlap_mlp_ = pj.value("overlap_mlp", getenv("IB2_NO_OVERLAP_MLP") == nullptr);
-  split_batch_ = pj.value("split_batch", getenv("IB2_NO_SPLIT_BATCH") == nullptr);
+  // Off by default: measured 5.7 % slower on C4 (46.5 vs 44.0 ms per
+  // iteration, profiles/r2e) -- the two chains contend for SMs (K1 fell from
+  // 0.94 to 0.70 of the HBM peak) and the weights are streamed twice.
+  split_batch_ = pj.value("split_batch", getenv("IB2_SPLIT_BATCH") != nullptr);
   trace_iters_ = pj.value("trace_iterations", false);
 
   roof_gbs_ = pj.value("roof_hbm_gbs", roof_gbs_);

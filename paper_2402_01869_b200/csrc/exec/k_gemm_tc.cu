@@ -409,12 +409,15 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
 //   warps 4-7   epilogue (both CTAs, own 128 rows).
 
 constexpr int kPairStages = 6;
+// BN: tile width (UMMA N of the pair); each CTA stages BN / 2 weight rows.
+template <int BN>
 struct PairSmem {
+  static constexpr int STAGES = BN == 256 ? kPairStages : 8;
   static constexpr int A_BYTES = 128 * BK * 2;
-  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = kPairStages * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * kPairStages + 4) * 8 + 16 + 1024;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
 };
 
 __device__ __forceinline__ std::uint32_t cta_rank_in_cluster() {
@@ -533,11 +536,12 @@ __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, flo
   }
 }
 
+template <int BN>
 __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_w,
                                                               GemmArgs args) {
-  using L = PairSmem;
-  constexpr int STAGES = kPairStages;
+  using L = PairSmem<BN>;
+  constexpr int STAGES = L::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
   std::uint64_t* full = reinterpret_cast<std::uint64_t*>(smem + L::BAR_OFF);
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
   const std::uint32_t rank = cta_rank_in_cluster();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int MT = (args.M + 255) / 256, NTL = (args.N + 255) / 256;
+  const int MT = (args.M + 255) / 256, NTL = (args.N + BN - 1) / BN;
   const int total = MT * NTL;
   const int nk = args.K / BK;
 
@@ -590,11 +594,16 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       // The weight tiles of the first ring's worth of k blocks stream in
       // before griddepcontrol.wait (they do not depend on the predecessor).
       int pre = 0;
+      // Row of this CTA's BN / 2 weight rows of tile ntl, k block kb, in the
+      // tile-blocked [N / 128][K / 64][128][64] weight layout.
+      auto wrow = [&](int ntl, int kb) {
+        return BN == 256 ? ((ntl * 2 + static_cast<int>(rank)) * nk + kb) * 128
+                         : (ntl * nk + kb) * 128 + static_cast<int>(rank) * 64;
+      };
       for (int t = pair; t < total && pre < STAGES && !args.no_early_w; t += npairs) {
-        const int wtile = (t / MT) * 2 + static_cast<int>(rank);
         for (int kb = 0; kb < nk && pre < STAGES; ++kb, ++pre) {
           if (leader) mbar_expect_tx(&full[pre], 2 * L::STAGE_BYTES);
-          tma_load_2d_pair(smem + pre * L::STAGE_BYTES + L::A_BYTES, &map_w, full0 + pre * 8, 0, (wtile * nk + kb) * 128);
+          tma_load_2d_pair(smem + pre * L::STAGE_BYTES + L::A_BYTES, &map_w, full0 + pre * 8, 0, wrow(t / MT, kb));
         }
       }
       pdl_wait();
@@ -602,7 +611,6 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       for (int t = pair; t < total; t += npairs) {
         const int mt = t % MT, ntl = t / MT;
         const int arow = mt * 256 + static_cast<int>(rank) * 128;
-        const int wtile = ntl * 2 + static_cast<int>(rank);  // this CTA's 128-row weight tile
         for (int kb = 0; kb < nk; ++kb, ++i) {
           const int st = i % STAGES;
           unsigned char* sa = smem + st * L::STAGE_BYTES;
@@ -614,20 +622,20 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
           mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
           if (leader) mbar_expect_tx(&full[st], 2 * L::STAGE_BYTES);
           tma_load_2d_pair(sa, &map_a, bar, kb * BK, arow);
-          tma_load_2d_pair(sa + L::A_BYTES, &map_w, bar, 0, (wtile * nk + kb) * 128);
+          tma_load_2d_pair(sa + L::A_BYTES, &map_w, bar, 0, wrow(ntl, kb));
         }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(256 >> 3) << 17) |
+      constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(BN >> 3) << 17) |
                                       (static_cast<std::uint32_t>(256 >> 4) << 24);
       int i = 0, seg = 0;
       for (int t = pair; t < total; t += npairs, ++seg) {
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const std::uint32_t acc_tmem = tmem + buf * 256;
+        const std::uint32_t acc_tmem = tmem + buf * BN;
         for (int kb = 0; kb < nk; ++kb, ++i) {
           const int st = i % STAGES;
           mbar_wait(&full[st], (i / STAGES) & 1);
@@ -670,13 +678,13 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       mbar_wait(&tfull[buf], (seg / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 16) {
+      for (int c = 0; c < BN; c += 16) {
         std::uint32_t r[16];
-        tmem_ld16(tmem + buf * 256 + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
+        tmem_ld16(tmem + buf * BN + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
         float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        epi_cols16(args, m, ntl * 256 + c, v);
+        epi_cols16(args, m, ntl * BN + c, v);
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
@@ -758,17 +766,18 @@ std::int64_t g_a_rows_capacity = 0;  // rows of every activation buffer (set by 
 
 int g_sms = 0;
 
-void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
-  using L = PairSmem;
+template <int BN>
+void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
+  using L = PairSmem<BN>;
   static bool configured = false;
   if (!configured) {
-    IB2_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
+    IB2_CUDA(cudaFuncSetAttribute(tc_gemm_pair_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL));
     configured = true;
   }
   const std::int64_t a_rows = a.a_rows > 0 ? a.a_rows : (g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, 128);
-  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, 128);
-  const int tiles = ((a.M + 255) / 256) * ((a.N + 255) / 256);
+  const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN / 2);
+  const int tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
   const int pairs = std::max(1, std::min(g_sms / 2, tiles));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
@@ -784,7 +793,24 @@ void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel, ma, mw, a));
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN>, ma, mw, a));
+}
+
+// Tile width by wave quantisation: the persistent pairs run ceil(tiles /
+// pairs) rounds of tiles; a 256 x 128 tile costs about half a 256 x 256 one.
+// N = 5120 at M ~ 1200 (O-proj, MLP-out of the 13B shape): 100 wide tiles on
+// 74 pairs = 2 rounds (68 % busy) vs 200 narrow = 3 half-rounds (90 %).
+int g_force_pair_bn = 0;  // isim_debug_gemm flags 4 / 8: force the 128 / 256 tile width
+
+void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
+  static const int env_force = getenv("IB2_PAIR_BN") ? atoi(getenv("IB2_PAIR_BN")) : 0;  // diagnostics
+  const int force = g_force_pair_bn ? g_force_pair_bn : env_force;
+  const int pairs = std::max(1, g_sms / 2), mt = (a.M + 255) / 256;
+  const int r256 = (mt * ((a.N + 255) / 256) + pairs - 1) / pairs;
+  const int r128 = (mt * ((a.N + 127) / 128) + pairs - 1) / pairs;
+  const bool narrow = force ? force == 128 : r128 < 2 * r256;
+  if (narrow) launch_tc_pair_bn<128>(a, s);
+  else launch_tc_pair_bn<256>(a, s);
 }
 
 // Work split of a decode-sized GEMM: clusters of S CTAs (K-slices) over T
@@ -956,6 +982,7 @@ void debug_tile_weights(const void* src, void* dst, int N, int K, void* stream) 
 void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, const void* bias, void* out, int ldo,
                 void* outf, int ldf, int flags, void* stream) {
   const bool force_simt = flags & 1;
+  g_force_pair_bn = (flags & 4) ? 128 : (flags & 8) ? 256 : 0;
   if (!(flags & 2)) {
   // The executor keeps weights tile-blocked; the hook takes row-major W.
   static f16* tiled = nullptr;
@@ -977,6 +1004,7 @@ void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, cons
   if (force_simt) launch_gemm_simt(g, s);
   else launch_gemm(g, s);
   g_a_rows_capacity = saved;
+  g_force_pair_bn = 0;
 }
 
 }  // namespace ib2

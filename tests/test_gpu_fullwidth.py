@@ -85,7 +85,8 @@ def test_fullwidth_parity_on_config_schedule(tmp_path, name):
     med = float(np.median([e[5] for e in errs]))
     assert med <= case["median"], med
     assert r["sampled"] > 50
-    assert r["ties"] <= max(2, r["sampled"] // 200)
+    # near-ties flip more often when the rounding floor is higher (13B shape)
+    assert r["ties"] <= max(2, int(r["sampled"] * case["rtol"] * 10))
     assert r["kv_checked"] > 0, "no swapped bytes were round-tripped"
     print(name, preset, f"{len(plans)} iterations, max recompute chunk {rec}, max context {ctx}, median err {med:.2e}",
           {k: v for k, v in r.items() if k != "stats"})

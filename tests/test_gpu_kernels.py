@@ -15,7 +15,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_gpu(), reason="needs 
 STORE, GELU, RESID, SWIGLU, STOREF32 = range(5)
 
 
-def run_gemm(a, w, epi, bias=None, resid=None, force_simt=False):
+def run_gemm(a, w, epi, bias=None, resid=None, force_simt=False, flags=0):
     import torch
     from paper_2402_01869_b200 import _abi
     M, K = a.shape
@@ -33,7 +33,7 @@ def run_gemm(a, w, epi, bias=None, resid=None, force_simt=False):
         a.data_ptr(), w.data_ptr(), M, N, K, epi, bias.data_ptr() if bias is not None else None,
         out.data_ptr() if out is not None else None, out.shape[1] if out is not None else 0,
         outf.data_ptr() if outf is not None else None, outf.shape[1] if outf is not None else 0,
-        1 if force_simt else 0, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        (1 if force_simt else 0) | flags, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     _abi.check(st)
     return out if out is not None else outf
 
@@ -77,6 +77,41 @@ def test_gemm_epilogues(M, N, K, epi):
     err = (got - ref).abs().max().item() / scale
     tol = 2e-3 if epi in (STORE, GELU, SWIGLU) else 1e-4  # fp16 output rounding vs fp32 outputs
     assert err <= tol, (M, N, K, epi, err)
+
+
+# Vicuna-13B projections (QKV, O, gate+up SwiGLU, down, LM head) at decode
+# (32), decode-heavy (200) and recompute-chunk (2048) batch sizes: the split-K
+# planner at 80 / 216 k-blocks and the CTA-pair kernel at both tile widths.
+SHAPES_13B = [(M, N, K, epi) for M in (32, 200, 2048)
+              for (N, K, epi) in ((15360, 5120, STORE), (5120, 5120, RESID), (27648, 5120, SWIGLU),
+                                  (5120, 13824, RESID), (32000, 5120, STOREF32))]
+
+
+def _check(M, N, K, epi, flags=0):
+    import torch
+    torch.manual_seed(M * 7 + N + K + epi)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
+    bias = (torch.randn(N, device="cuda") * 0.02).half() if epi != SWIGLU else None
+    resid = torch.randn(M, N, device="cuda") if epi == RESID else None
+    got = run_gemm(a, w, epi, bias, resid, flags=flags).float()
+    ref = reference(a, w, epi, bias, resid).float()
+    scale = ref.abs().max().item() + 1e-6
+    err = (got - ref).abs().max().item() / scale
+    tol = 2e-3 if epi in (STORE, GELU, SWIGLU) else 1e-4
+    assert err <= tol, (M, N, K, epi, flags, err)
+
+
+@pytest.mark.parametrize("M,N,K,epi", SHAPES_13B)
+def test_gemm_13b_shapes(M, N, K, epi):
+    _check(M, N, K, epi)
+
+
+@pytest.mark.parametrize("flags", [4, 8])
+@pytest.mark.parametrize("M,N,K,epi", [(1218, 5120, 5120, RESID), (1218, 15360, 5120, STORE),
+                                       (513, 27648, 5120, SWIGLU), (300, 1000, 512, GELU), (2048, 32000, 5120, STOREF32)])
+def test_pair_gemm_tile_widths(M, N, K, epi, flags):
+    _check(M, N, K, epi, flags)
 
 
 @pytest.mark.parametrize("M,N,K", [(77, 1024, 1024), (640, 4096, 4096)])

@@ -73,7 +73,9 @@ def replay(plans, model, pools, n_iters, check_tables_every=1, kv_check=True, er
                     errors.append((plan_j["it"], sp[0], sp[3], sp[2], sp[1], err))
                 assert err <= rtol, f"iteration {plan_j['it']} row {i}: logits rel err {err:.2e}"
                 if t != ref["tokens"][i]:
-                    assert ref["margin"][i] <= TIE_FRAC * scale, (plan_j["it"], i, t, ref["tokens"][i], ref["margin"][i])
+                    # a flip needs a top-2 margin within the two logits' combined error
+                    assert ref["margin"][i] <= TIE_FRAC * (rtol / LOGIT_RTOL) * scale, \
+                        (plan_j["it"], i, t, ref["tokens"][i], ref["margin"][i])
                     ties += 1
                 sampled += 1
         if kv_check:
