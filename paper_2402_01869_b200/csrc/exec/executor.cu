@@ -1001,7 +1001,8 @@ void Impl::consume(const isim_batch_plan& p) {
     std::int64_t work = 0;
     for (const TileDesc& t : tiles) work += static_cast<std::int64_t>(t.pos0 + t.nrows) * H;
     static const int min_keys = getenv("IB2_K2_MIN_KEYS") ? atoi(getenv("IB2_K2_MIN_KEYS")) : 2 * bn;
-    std::int64_t per = std::max<std::int64_t>(min_keys, (work + 147) / 148);
+    const std::int64_t slots = 148LL * chunk_attention_ctas_per_sm(spec_.head_dim());
+    std::int64_t per = std::max<std::int64_t>(min_keys, (work + slots - 1) / slots);
     per = (per + bn - 1) / bn * bn;
     int parts = 0;
     for (const TileDesc& t : tiles) {

@@ -24,6 +24,7 @@
 // Keys are visited in ascending block order, like K1.  Tensor-core
 // bound: 4 * rows * keys * hd FLOP per (item, head).
 #include <cfloat>
+#include <cstdio>
 #include <mutex>
 #include <unordered_map>
 
@@ -45,28 +46,39 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O when the max grew by > 2^8
 
+// Head dims 64 / 128 run two CTAs per SM (64-key tiles, 256 TMEM columns
+// and <= 113 KB of shared memory each; head dim 128 with one P buffer): the
+// two CTAs' softmax warps interleave on the SM while either one's MMAs run,
+// which one CTA's four softmax warps cannot keep busy.  Head dim 256 (O alone
+// takes 256 columns) keeps one CTA per SM with 64-key tiles.
 template <int HD>
 struct AttnCfg {
   static constexpr int BQ = 128;
-  static constexpr int BN = HD == 256 ? 64 : 128;  // keys per tile
-  static constexpr int NCH = HD / 64;              // 64-wide head-dim chunks (one 128 B swizzle row)
+  static constexpr int BN = 64;                     // keys per tile
+  static constexpr int CTAS = HD == 256 ? 1 : 2;    // resident CTAs per SM
+  static constexpr int NP = HD == 128 ? 1 : 2;      // P buffers
+  static constexpr int NCH = HD / 64;               // 64-wide head-dim chunks (one 128 B swizzle row)
   static constexpr int STAGES = 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BN * HD * 2;  // K or V tile
   static constexpr int STAGE_BYTES = 2 * KV_BYTES;
-  static constexpr int P_BYTES = BQ * BN * 2;  // one of two P buffers
+  static constexpr int P_BYTES = BQ * BN * 2;  // one P buffer
   static constexpr int KV_OFF = Q_BYTES;
   static constexpr int P_OFF = KV_OFF + STAGES * STAGE_BYTES;
-  static constexpr int BAR_OFF = P_OFF + 2 * P_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 256 + 1024;  // barriers + alignment slack
-  static constexpr int TMEM_COLS = 512;
+  static constexpr int BAR_OFF = P_OFF + NP * P_BYTES;
+  // Barriers + alignment slack.  Two CTAs per SM must fit in 228 KB minus
+  // 1 KB reserved per CTA (115,712 B each): the slack assumes the dynamic
+  // shared window starts at least 512 B aligned (checked in the kernel).
+  static constexpr int SLACK = 512;
+  static constexpr int TOTAL = BAR_OFF + 256 + SLACK;
+  static constexpr int TMEM_COLS = CTAS == 2 ? 256 : 512;
   static constexpr int S_COL = HD;  // S buffers after O
   static_assert(HD + 2 * BN <= TMEM_COLS, "TMEM budget");
-  static_assert(TOTAL <= 232448, "shared memory budget");
+  static_assert(CTAS == 1 ? TOTAL <= 232448 : TOTAL <= 115712, "shared memory budget");
 };
 
 template <int HD>
-__global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap map_q,
+__global__ void __launch_bounds__(256, AttnCfg<HD>::CTAS) chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap map_q,
                                                                const __grid_constant__ CUtensorMap map_kv,
                                                                const TileDesc* __restrict__ items,
                                                                const std::int32_t* __restrict__ table, int max_lb,
@@ -74,7 +86,7 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
                                                                f16* __restrict__ out, float* __restrict__ ws_o,
                                                                float* __restrict__ ws_ml) {
   using C = AttnCfg<HD>;
-  constexpr int BQ = C::BQ, BN = C::BN, NCH = C::NCH, STAGES = C::STAGES;
+  constexpr int BQ = C::BQ, BN = C::BN, NCH = C::NCH, STAGES = C::STAGES, NP = C::NP;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -86,12 +98,13 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
   std::uint64_t* vempty = vfull + STAGES;   // [STAGES] PV MMA done with it
   std::uint64_t* sfull = vempty + STAGES;   // [2]
   std::uint64_t* sfree = sfull + 2;         // [2]
-  std::uint64_t* pfull = sfree + 2;         // [2] P buffer written (4 warps)
-  std::uint64_t* pvdone = pfull + 2;        // [2] PV MMA of that P buffer done
+  std::uint64_t* pfull = sfree + 2;         // [NP] P buffer written (4 warps)
+  std::uint64_t* pvdone = pfull + 2;        // [NP] PV MMA of that P buffer done
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(pvdone + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.y;
+  if (threadIdx.x == 0 && smem - smem_raw > C::SLACK) __trap();  // layout would overrun the allocation
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_q);
@@ -168,8 +181,8 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
       constexpr std::uint32_t idesc_pv = idesc_f16(BQ, HD, false, true);
       const std::uint32_t q_base = su32(sQ), kv_base = su32(sKV), p_base = su32(sP);
       auto issue_pv = [&](int u) {
-        const int pb = u & 1, st = u % STAGES;
-        mbar_wait(&pfull[pb], (u / 2) & 1);
+        const int pb = u % NP, st = u % STAGES;
+        mbar_wait(&pfull[pb], (u / NP) & 1);
         mbar_wait(&vfull[st], (u / STAGES) & 1);
         fence_after();
         const std::uint32_t v_base = kv_base + st * C::STAGE_BYTES + C::KV_BYTES;
@@ -272,12 +285,12 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
         l += back.x + back.y;
         pk[i / 2] = *reinterpret_cast<const std::uint32_t*>(&hv);
       }
-      // P buffer t&1 is free once PV(t-2) retired; O may only be rescaled
+      // P buffer t%NP is free once PV(t-NP) retired; O may only be rescaled
       // after PV(t-1) (which accumulates into it) and before PV(t).
-      const int pbuf = t & 1;
-      if (t >= 2) mbar_wait(&pvdone[pbuf], ((t - 2) / 2) & 1);
+      const int pbuf = t % NP;
+      if (t >= NP) mbar_wait(&pvdone[pbuf], ((t - NP) / NP) & 1);
       if (__any_sync(0xffffffffu, rescale)) {
-        if (t >= 1) mbar_wait(&pvdone[(t - 1) & 1], ((t - 1) / 2) & 1);
+        if (t >= 1) mbar_wait(&pvdone[(t - 1) % NP], ((t - 1) / NP) & 1);
         fence_after();
 #pragma unroll 1
         for (int c = 0; c < HD; c += 16) {
@@ -309,7 +322,7 @@ __global__ void __launch_bounds__(256, 1) chunk_attn_tc_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(&pfull[pbuf]);
     }
     // Epilogue.
-    mbar_wait(&pvdone[(nt - 1) & 1], ((nt - 1) / 2) & 1);
+    mbar_wait(&pvdone[(nt - 1) % NP], ((nt - 1) / NP) & 1);
     fence_after();
     if (td.part < 0) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -425,6 +438,13 @@ void launch_chunk_hd(const f16* qkv, int qkv_rows, const TileDesc* items, int n_
   static bool configured = false;
   if (!configured) {
     IB2_CUDA(cudaFuncSetAttribute(chunk_attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::TOTAL));
+    // Two CTAs per SM need the whole 228 KB carve-out for shared memory.
+    IB2_CUDA(cudaFuncSetAttribute(chunk_attn_tc_kernel<HD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  cudaSharedmemCarveoutMaxShared));
+    int per_sm = 0;
+    IB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_attn_tc_kernel<HD>, 256, C::TOTAL));
+    if (per_sm < C::CTAS)
+      fprintf(stderr, "chunk_attn_tc_kernel<%d>: %d resident CTAs per SM, planned %d\n", HD, per_sm, C::CTAS);
     configured = true;
   }
   const std::int64_t layer_row0 = static_cast<std::int64_t>(layer) * g.num_blocks * 2 * g.heads * kBlockTokens;
@@ -434,6 +454,15 @@ void launch_chunk_hd(const f16* qkv, int qkv_rows, const TileDesc* items, int n_
 }
 
 }  // namespace
+
+int chunk_attention_ctas_per_sm(int head_dim) {
+  switch (head_dim) {
+    case 64: return AttnCfg<64>::CTAS;
+    case 128: return AttnCfg<128>::CTAS;
+    case 256: return AttnCfg<256>::CTAS;
+    default: throw DeviceError("unsupported head_dim");
+  }
+}
 
 int chunk_attention_key_tile(int head_dim) {
   switch (head_dim) {

@@ -151,6 +151,17 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, i
 // Per row: rotate q and k of every head (fp32, no contraction, matching the
 // oracle's float32 arithmetic), round to f16, and store k, v into the row's
 // paged slot.
+// K4: RoPE on q and k + k, v into the paged pool, 16-byte vectors.  Work
+// items per row: q / k rotated vectors (rotate-half: one item = a vector of
+// the first half and its partner in the second, so q can be updated in place;
+// interleaved: one item = one vector of adjacent pairs), the unrotated k
+// dims, and v.  k and v go straight to the pool (K1 / K2 read them there);
+// only q is written back to the qkv rows.
+__device__ __forceinline__ void rot_pair(float a, float b, float co, float si, float& ra, float& rb) {
+  ra = __fsub_rn(__fmul_rn(a, co), __fmul_rn(b, si));
+  rb = __fadd_rn(__fmul_rn(b, co), __fmul_rn(a, si));
+}
+
 __global__ void rope_kv_kernel(f16* __restrict__ qkv, const RowDesc* __restrict__ rows, f16* __restrict__ pool,
                                std::int64_t layer_off, std::int64_t block_stride, const std::int32_t* __restrict__ table,
                                int max_lb, int H, int hd, int rot, int interleaved, const float* __restrict__ cs) {
@@ -163,33 +174,64 @@ __global__ void rope_kv_kernel(f16* __restrict__ qkv, const RowDesc* __restrict_
   const int pb = table[static_cast<std::int64_t>(d.slot) * max_lb + d.pos / kBlockTokens];
   f16* blk = pool + layer_off + static_cast<std::int64_t>(pb) * block_stride;
   const int tok = d.pos % kBlockTokens;
-  const int half = rot / 2;
-  const float* c = cs + static_cast<std::int64_t>(d.pos) * rot;  // [half][2] = (cos, sin)
-  // q and k rotations: H heads x half pairs each.
-  for (int t = threadIdx.x; t < 2 * H * half; t += blockDim.x) {
-    const int which = t / (H * half);  // 0 = q, 1 = k
-    const int h = (t / half) % H;
-    const int i = t % half;
-    f16* base = row + which * D + h * hd;
-    const int ia = interleaved ? 2 * i : i;
-    const int ib = interleaved ? 2 * i + 1 : i + half;
-    const float a = __half2float(base[ia]), b = __half2float(base[ib]);
-    const float co = c[2 * i], si = c[2 * i + 1];
-    const float ra = __fsub_rn(__fmul_rn(a, co), __fmul_rn(b, si));
-    const float rb = __fadd_rn(__fmul_rn(b, co), __fmul_rn(a, si));
-    base[ia] = __float2half_rn(ra);
-    base[ib] = __float2half_rn(rb);
-  }
-  __syncthreads();
-  // k, v -> pool [kv][h][tok][hd], 16-byte vectors.
-  const int vec = hd / 8;
-  for (int t = threadIdx.x; t < 2 * H * vec; t += blockDim.x) {
-    const int kv = t / (H * vec);
-    const int h = (t / vec) % H;
-    const int j = t % vec;
-    const uint4 val = *reinterpret_cast<const uint4*>(row + (1 + kv) * D + h * hd + j * 8);
-    f16* dst = blk + ((static_cast<std::int64_t>(kv) * H + h) * kBlockTokens + tok) * hd + j * 8;
-    *reinterpret_cast<uint4*>(dst) = val;
+  const float* c = cs + static_cast<std::int64_t>(d.pos) * rot;  // [rot/2][2] = (cos, sin)
+  const int vec = hd / 8, rvec = rot / 8;             // 16 B vectors per head / rotated ones
+  const int ritems = interleaved ? rvec : rvec / 2;   // rotation items per head
+  auto kv_dst = [&](int kv, int h, int j) {
+    return reinterpret_cast<uint4*>(blk + ((static_cast<std::int64_t>(kv) * H + h) * kBlockTokens + tok) * hd + j * 8);
+  };
+  const int n_rot = 2 * H * ritems;          // q and k rotation items
+  const int n_kcopy = H * (vec - rvec);      // unrotated k vectors
+  const int n_v = H * vec;
+  for (int t = threadIdx.x; t < n_rot + n_kcopy + n_v; t += blockDim.x) {
+    if (t < n_rot) {
+      const int which = t / (H * ritems);  // 0 = q, 1 = k
+      const int h = (t / ritems) % H, j = t % ritems;
+      f16* head = row + which * D + h * hd;
+      if (interleaved) {
+        uint4 u = *reinterpret_cast<const uint4*>(head + j * 8);
+        __half2* hp = reinterpret_cast<__half2*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int i = j * 4 + e;
+          const float2 ab = __half22float2(hp[e]);
+          float ra, rb;
+          rot_pair(ab.x, ab.y, c[2 * i], c[2 * i + 1], ra, rb);
+          hp[e] = __halves2half2(__float2half_rn(ra), __float2half_rn(rb));
+        }
+        if (which == 0) *reinterpret_cast<uint4*>(head + j * 8) = u;
+        else *kv_dst(0, h, j) = u;
+      } else {
+        const int half = rot / 2, jb = j + half / 8;
+        uint4 ua = *reinterpret_cast<const uint4*>(head + j * 8);
+        uint4 ub = *reinterpret_cast<const uint4*>(head + jb * 8);
+        __half* ha = reinterpret_cast<__half*>(&ua);
+        __half* hb = reinterpret_cast<__half*>(&ub);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = j * 8 + e;
+          float ra, rb;
+          rot_pair(__half2float(ha[e]), __half2float(hb[e]), c[2 * i], c[2 * i + 1], ra, rb);
+          ha[e] = __float2half_rn(ra);
+          hb[e] = __float2half_rn(rb);
+        }
+        if (which == 0) {
+          *reinterpret_cast<uint4*>(head + j * 8) = ua;
+          *reinterpret_cast<uint4*>(head + jb * 8) = ub;
+        } else {
+          *kv_dst(0, h, j) = ua;
+          *kv_dst(0, h, jb) = ub;
+        }
+      }
+    } else if (t < n_rot + n_kcopy) {
+      const int u = t - n_rot, nv = vec - rvec;
+      const int h = u / nv, j = rvec + u % nv;
+      *kv_dst(0, h, j) = *reinterpret_cast<const uint4*>(row + D + h * hd + j * 8);
+    } else {
+      const int u = t - n_rot - n_kcopy;
+      const int h = u / vec, j = u % vec;
+      *kv_dst(1, h, j) = *reinterpret_cast<const uint4*>(row + 2 * D + h * hd + j * 8);
+    }
   }
 }
 
@@ -374,6 +416,8 @@ void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, 
 void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g, int layer, int rotary_dim,
                           bool interleaved, const float* rope_cs, cudaStream_t s) {
   if (n <= 0) return;
+  if (g.head_dim % 8 || rotary_dim % (interleaved ? 8 : 16) || rotary_dim > g.head_dim)
+    throw DeviceError("rope_kv: head_dim / rotary_dim not a multiple of the 16-byte vector");
   launch_pdl(rope_kv_kernel, dim3(n), dim3(256), 0, s, qkv, rows, g.pool, layer * g.layer_stride(), g.block_stride(),
              g.table, g.max_lblocks, g.heads, g.head_dim, rotary_dim, interleaved ? 1 : 0, rope_cs);
   IB2_LAUNCH_CHECK();

@@ -53,6 +53,8 @@ void launch_chunk_attention(const f16* qkv, int qkv_rows, const TileDesc* items,
                             float* ws_o, float* ws_ml, cudaStream_t s);
 // Keys per K2 tile for a head dim (split-KV ranges are aligned to it).
 int chunk_attention_key_tile(int head_dim);
+// Resident K2 CTAs per SM for a head dim (the split-KV planner's slot count).
+int chunk_attention_ctas_per_sm(int head_dim);
 
 // 2-D f16 TMA descriptor over [rows][inner] (row stride in bytes), box
 // box_inner x box_rows, 128-byte swizzle.
