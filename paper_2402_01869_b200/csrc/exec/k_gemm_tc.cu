@@ -796,20 +796,18 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN>, ma, mw, a));
 }
 
-// Tile width by wave quantisation: the persistent pairs run ceil(tiles /
-// pairs) rounds of tiles; a 256 x 128 tile costs about half a 256 x 256 one.
-// N = 5120 at M ~ 1200 (O-proj, MLP-out of the 13B shape): 100 wide tiles on
-// 74 pairs = 2 rounds (68 % busy) vs 200 narrow = 3 half-rounds (90 %).
 int g_force_pair_bn = 0;  // isim_debug_gemm flags 4 / 8: force the 128 / 256 tile width
 
+// Tile width.  256 x 256 always: the 256 x 128 tile was meant to cut wave
+// quantisation (N = 5120 at M ~ 1200: 100 wide tiles on 74 pairs = 2 rounds,
+// 68 % busy) but measured 30-45 % slower per GEMM on every 13B projection at
+// M = 600 / 1218 / 2048 (profiles/r2g/gemm_tile_width.txt) -- a 256 x 128 k
+// step halves the MMA work but not the per-stage barrier / TMA cost.  It stays
+// selectable for tests (isim_debug_gemm flag 4) and diagnostics (IB2_PAIR_BN).
 void launch_tc_pair(const GemmArgs& a, cudaStream_t s) {
   static const int env_force = getenv("IB2_PAIR_BN") ? atoi(getenv("IB2_PAIR_BN")) : 0;  // diagnostics
   const int force = g_force_pair_bn ? g_force_pair_bn : env_force;
-  const int pairs = std::max(1, g_sms / 2), mt = (a.M + 255) / 256;
-  const int r256 = (mt * ((a.N + 255) / 256) + pairs - 1) / pairs;
-  const int r128 = (mt * ((a.N + 127) / 128) + pairs - 1) / pairs;
-  const bool narrow = force ? force == 128 : r128 < 2 * r256;
-  if (narrow) launch_tc_pair_bn<128>(a, s);
+  if (force == 128) launch_tc_pair_bn<128>(a, s);
   else launch_tc_pair_bn<256>(a, s);
 }
 
