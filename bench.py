@@ -56,9 +56,18 @@ ALL6 = [{"name": c} for c in ["Math", "QA", "VE", "Chatbot", "Image", "TTS"]]
 GPTJ_M, M13 = 458752, 819200
 RUN = {"policy": "infercept", "estimator": "oracle"}
 
-# SURVEY §8d configurations (C0 is the tiny CPU-runnable case, tests only).
+# SURVEY §8d configurations.
 CONFIGS = {
-    "C1": dict(model={"preset": "gptj-6b"}, layers=28, M=GPTJ_M,
+    "C0": dict(l2="inputs fit in L2 (64 MiB KV pool): the tiny CPU-runnable case, not a headline", model={"preset": "tiny"}, layers=2, M=4096,
+               workload=dict(classes=[{"name": c} for c in ["Math", "QA", "VE", "Chatbot", "Image", "TTS"]],
+                             request_count=64, arrival_rate=1.0, seed=1, max_seq_len=4096),
+               cost=dict(t0=2e-3, slope_below=1e-6, slope_above=1e-5, saturation_point=512, mem_per_token=4096,
+                         gpu_kv_capacity=16384 * 4096, cpu_kv_capacity=4 * 16384 * 4096, swap_per_token=8.192e-6,
+                         block_size=16),
+               slack_blocks=512,
+               name="C0: tiny GPT (2 layers, d=256, 4 heads, fp32 cost model M=4096), 64-request trace of all six "
+                    "API classes (seed 1), InferCept min-waste policy, 64 MiB GPU / 256 MiB CPU KV ledger"),
+    "C1": dict(l2="inputs larger than L2 (150 GB KV pool, ~15 GB of KV read per iteration)", model={"preset": "gptj-6b"}, layers=28, M=GPTJ_M,
                workload=dict(classes=[{"name": "Math"}, {"name": "QA"}, {"name": "Chatbot"}], request_count=2000,
                              arrival_rate=3.0, seed=11),
                cost=dict(mem_per_token=GPTJ_M, gpu_kv_capacity=150e9, cpu_kv_capacity=128e9,
@@ -66,21 +75,21 @@ CONFIGS = {
                slack_blocks=512,
                name="C1: GPT-J-6B-shaped random-init fp16 model, Math/QA/Chatbot API trace (2000 req @3/s, seed 11), "
                     "InferCept min-waste policy, reference cost-model defaults, 150 GB GPU / 128 GB CPU KV ledger"),
-    "C2": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+    "C2": dict(l2="inputs larger than L2 (120 GB KV pool)", model={"preset": "vicuna-13b"}, layers=40, M=M13,
                workload=dict(classes=[{"name": "Chatbot"}, {"name": "VE"}], request_count=1000, arrival_rate=2.0,
                              seed=13),
                cost=dict(mem_per_token=M13, gpu_kv_capacity=120e9, cpu_kv_capacity=96e9, swap_per_token=M13 / LINK),
                slack_blocks=512,
                name="C2: Vicuna-13B-shaped model, Chatbot + VE trace (1000 req @2/s, seed 13), 120 GB / 96 GB ledger: "
                     "chunked swap under the swap budget"),
-    "C3": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+    "C3": dict(l2="inputs larger than L2 (40 GB KV pool, 3k-token contexts)", model={"preset": "vicuna-13b"}, layers=40, M=M13,
                workload=dict(classes=[{"name": "QA", "context_mean": 3000.0, "context_var": 200.0 ** 2}],
                              request_count=1000, arrival_rate=2.0, seed=17),
                cost=dict(mem_per_token=M13, gpu_kv_capacity=40e9, cpu_kv_capacity=128e9, swap_per_token=M13 / LINK),
                slack_blocks=512,
                name="C3: Vicuna-13B-shaped model, QA-shaped calls over 3000-token contexts (1000 req @2/s, seed 17), "
                     "40 GB GPU ledger: Discard-heavy chunked recompute"),
-    "C4": dict(model={"preset": "vicuna-13b"}, layers=40, M=M13,
+    "C4": dict(l2="inputs larger than L2 (140 GB KV pool, tens of GB of KV read per iteration)", model={"preset": "vicuna-13b"}, layers=40, M=M13,
                workload=dict(classes=ALL6, request_count=4000, arrival_rate=1000.0, seed=23),
                cost=dict(mem_per_token=M13, gpu_kv_capacity=140e9, cpu_kv_capacity=64e9, swap_per_token=M13 / LINK),
                slack_blocks=64,  # 140 GB pool + 26 GB of weights: little room for slack
@@ -260,12 +269,17 @@ def run_b200(args):
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DEVICE pins every rank to one device (tests of the N > 1 plumbing
+    # on a single GPU with a small config); normally rank = local GPU.
+    local = int(os.environ.get("BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if "BENCH_DEVICE" in os.environ:  # ranks share one GPU: NCCL refuses duplicate devices
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     link = measure_link(torch)
     pk = peaks()
     tmp = tempfile.mkdtemp()
@@ -362,7 +376,7 @@ def run_b200(args):
                                 "are a stratified sample of each schedule",
                    "windows": [[s, c] for s, c in wins], "warmup_per_window": args.warmup,
                    "schedule_iterations": [g["iters"] for g in gathered],
-                   "l2": "inputs larger than L2 (140 GB KV pool, tens of GB of KV read per iteration)"},
+                   "l2": cfg["l2"]},
         "decode_tok_s": tot["decode"] / dev_s_max,
         "completed_in_windows": tot["completed"],
         "replay_seconds_estimated": max(replay),
@@ -438,13 +452,39 @@ def cpu_forward_seconds(preset, layers_total, plans, reps=2):
     return per_iter, dict(t1=t1, t2=t2, spread=spread, cores=cores, runs=per_layers)
 
 
+def cpu_full_trace_seconds(preset, plans):
+    """Whole-trace CPU time of the numpy fp32 oracle forward at full depth
+    (every iteration of the schedule, all host threads): measured, not
+    extrapolated.  Only sensible for the tiny C0 model."""
+    from threadpoolctl import threadpool_limits
+    from oracle.forward import ForwardOracle
+    with threadpool_limits(limits=os.cpu_count()):
+        fo = ForwardOracle({"preset": preset}, precision="f32")
+        t = time.perf_counter()
+        for pj in plans:
+            fo._forward_only(pj)
+        return (time.perf_counter() - t) / len(plans)
+
+
 def cpu_reference(cfg, args, wins):
     """The reference's CPU path on this host (see module docstring)."""
     from oracle.ref_plans import reference_schedule, run_reference as ref_run
-    keep = {s + 1 for s, _ in wins}  # event-log iteration numbers are 1-based
+    full = getattr(args, "full_trace", False)
+    keep = None if full else {s + 1 for s, _ in wins}  # event-log iteration numbers are 1-based
     with tempfile.TemporaryDirectory() as d:
         summ, plans = reference_schedule(cfg["workload"], cfg["cost"], RUN, keep=keep, workdir=d)
     t_sched = ref_run(cfg["workload"], cfg["cost"], RUN, None)["wall_s"] / summ["iterations"]
+    if full:
+        fwd = cpu_full_trace_seconds(cfg["model"]["preset"], plans)
+        per_iter = fwd + t_sched
+        value = summ["done_events"] / (summ["iterations"] * per_iter)
+        return {"value": value, "s_per_iteration": per_iter, "cores": os.cpu_count(), "iterations": summ["iterations"],
+                "completed": summ["done_events"], "sched_us_per_iteration": t_sched * 1e6,
+                "forward": {"runs": {str(cfg["layers"]): [fwd]}},
+                "sample": (f"reference engine (oracle/_ref, {t_sched * 1e6:.1f} us/iteration) + numpy fp32 oracle "
+                           f"forward of EVERY one of the {len(plans)} iterations at full depth (batches recovered "
+                           f"from the reference's event log): {per_iter * 1e3:.2f} ms/iteration, measured over the "
+                           f"whole trace")}
     per_iter, det = cpu_forward_seconds(cfg["model"]["preset"], cfg["layers"], plans)
     per_iter += t_sched
     value = summ["done_events"] / (summ["iterations"] * per_iter)
@@ -473,11 +513,13 @@ def run_reference(args):
         "metric": METRIC, "value": v, "unit": "req/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": cpu["s_per_iteration"] * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (numpy)", "data": "synthetic", "impl": "reference",
-        "extrapolated": True,
+        "extrapolated": not args.full_trace and cfg["layers"] > 2,
         "config": {"workload": cfg["name"], "config": args.config,
                    "host": "rank 0 only, all host threads, the whole (unsharded) trace; no GPU used",
                    "estimator": "value = requests / (iterations of the reference schedule x CPU seconds per "
-                                "iteration), the per-iteration time sampled at the B200 arm's window positions",
+                                "iteration), the per-iteration time " +
+                                ("measured over every iteration of the trace" if args.full_trace else
+                                 "sampled at the B200 arm's window positions"),
                    "windows": [[s, c] for s, c in wins]},
         "cpu_baseline": {"value": v, "unit": "req/s", "cores": cpu["cores"], "kind": "port",
                          "sample": cpu["sample"]},
@@ -497,6 +539,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host pool per rank (default: ledger x 1.25)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--full-trace", action="store_true",
+                    help="CPU path: time the oracle forward over every iteration (C0 only: minutes)")
     ap.add_argument("--gpu-blocks", type=int, default=0,
                     help="override the KV pool size (profiling runs only; the scheduler's capacity is unchanged)")
     args = ap.parse_args()

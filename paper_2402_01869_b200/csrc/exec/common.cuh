@@ -158,6 +158,7 @@ struct GemmArgs {
   int no_early_w;      // diagnostics: no weight prefetch before griddepcontrol.wait
   const float* addf;   // Epi::ResidAdd: if set, outf = (outf + acc) + addf (same [M][ldf] layout)
   std::int64_t a_rows;  // rows addressable from `a` for TMA bounds (0: the executor's buffer capacity)
+  int streamk_ok;       // decode GEMM may use stream-K (only where no other stream-K GEMM runs concurrently)
 };
 
 }  // namespace ib2

@@ -1204,6 +1204,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
     GemmArgs ga{a, weights_ + w, M, N, K, epi, W(bias), out, ldo, outf, ldf};
     ga.addf = addf;
     ga.a_rows = max_rows_ - off;  // TMA bounds of an A operand that starts at row `off`
+    ga.streamk_ok = st == main_ ? 1 : 0;
     launch_gemm(ga, st);
     ++kernel_launches_;
   };

@@ -8,13 +8,13 @@
 //   warp 0      TMA producer: the Q tile once ([128][hd] from the qkv
 //               activations), then per key tile the K and V rows of BN/16 paged
 //               blocks ([16][hd] each, contiguous in the pool) into a 2-stage
-//               ring, 128-byte swizzle;
+//               ring, 128-byte swizzle (64-key tiles);
 //   warp 1      MMA issuer: S_t = Q K_t^T (M=128, N=BN, K=hd; both operands
 //               K-major) into one of two TMEM S buffers, then O += P_{t-1} V_{t-1}
 //               (M=128, N=hd, K=BN; P K-major from shared memory, V MN-major
 //               straight from the TMA tile) -- S_t overlaps softmax(t-1);
-//   warp 2      TMEM allocator (512 columns: O = hd, S = 2 x BN);
-//   warps 4-7   softmax: thread = query row = TMEM lane.  Row max / exp2 / sum
+//   warps 2-5   softmax (warp 2 also allocates TMEM: O = hd, S = 2 x BN
+//               columns): thread = query row = TMEM lane.  Row max / exp2 / sum
 //               are thread-local (no shuffles); P is written f16 into swizzled
 //               shared memory; O is rescaled in TMEM only when the running max
 //               grew by more than 2^8 (the exact max used is tracked, so the
@@ -45,6 +45,10 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: rescale O when the max grew by > 2^8
+// Six warps: 0 TMA producer, 1 MMA issuer, 2-5 softmax (2 also allocates
+// TMEM).  192 threads x <= 128 registers lets two CTAs share an SM's 64K
+// registers (256 threads did not: 1 resident CTA).
+constexpr int kK2Threads = 192;
 
 // Head dims 64 / 128 run two CTAs per SM (64-key tiles, 256 TMEM columns
 // and <= 113 KB of shared memory each; head dim 128 with one P buffer): the
@@ -78,7 +82,7 @@ struct AttnCfg {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(256, AttnCfg<HD>::CTAS) chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap map_q,
+__global__ void __launch_bounds__(kK2Threads, AttnCfg<HD>::CTAS) chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap map_q,
                                                                const __grid_constant__ CUtensorMap map_kv,
                                                                const TileDesc* __restrict__ items,
                                                                const std::int32_t* __restrict__ table, int max_lb,
@@ -215,8 +219,10 @@ __global__ void __launch_bounds__(256, AttnCfg<HD>::CTAS) chunk_attn_tc_kernel(c
       }
       issue_pv(nt - 1);
     }
-  } else if (warp >= 4) {
-    const int q = warp - 4;
+  } else {
+    // warps 2-5: TMEM lane quarter = warp % 4 (a warp reaches only lanes
+    // 32 * (warp % 4) .. + 31), so the four quarters are 2, 3, 0, 1.
+    const int q = warp & 3;
     const int r = q * 32 + lane;  // query row of this thread = TMEM lane
     const std::uint32_t lane_off = static_cast<std::uint32_t>(q * 32) << 16;
     const int qp = td.pos0 + min(r, td.nrows - 1);
@@ -441,14 +447,14 @@ void launch_chunk_hd(const f16* qkv, int qkv_rows, const TileDesc* items, int n_
     // Two CTAs per SM need the whole 228 KB carve-out for shared memory.
     IB2_CUDA(cudaFuncSetAttribute(chunk_attn_tc_kernel<HD>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                   cudaSharedmemCarveoutMaxShared));
-    int per_sm = 0;
-    IB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, chunk_attn_tc_kernel<HD>, 256, C::TOTAL));
-    if (per_sm < C::CTAS)
-      fprintf(stderr, "chunk_attn_tc_kernel<%d>: %d resident CTAs per SM, planned %d\n", HD, per_sm, C::CTAS);
+    // (cudaOccupancyMaxActiveBlocksPerMultiprocessor answers 1 for any kernel
+    // that uses tcgen05.alloc, but the hardware co-schedules two such CTAs
+    // per SM when their TMEM allocations fit: tools/occ/occ4.cu measured 148
+    // of 148 SMs running two 256-column CTAs at once.)
     configured = true;
   }
   const std::int64_t layer_row0 = static_cast<std::int64_t>(layer) * g.num_blocks * 2 * g.heads * kBlockTokens;
-  launch_pdl(chunk_attn_tc_kernel<HD>, dim3(n_items, g.heads), dim3(256), C::TOTAL, s, q_map(qkv, qkv_rows, g.heads * HD),
+  launch_pdl(chunk_attn_tc_kernel<HD>, dim3(n_items, g.heads), dim3(kK2Threads), C::TOTAL, s, q_map(qkv, qkv_rows, g.heads * HD),
              kv_map(g), items, g.table, g.max_lblocks, layer_row0, g.heads, out, ws_o, ws_ml);
   IB2_LAUNCH_CHECK();
 }

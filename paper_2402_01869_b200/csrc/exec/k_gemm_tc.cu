@@ -202,10 +202,34 @@ __device__ __forceinline__ void arrive_remote(std::uint32_t cluster_addr) {
 }
 __device__ __forceinline__ void wait_cluster(std::uint64_t* b, std::uint32_t parity) { mbar_wait_cluster(b, parity); }
 
+// Stream-K (S = 1, sk != nullptr): the (tile, k block) units are split
+// evenly over the grid, so every SM streams the same number of weight bytes
+// whatever the tile count (96 / 128 / 394 GPT-J tiles on 148 SMs).  A CTA's
+// range is a run of segments: maybe the END of one tile (its first segment,
+// kb > 0), whole tiles, maybe the START of a tile (its last segment).  The
+// CTA holding a tile's k block 0 owns it and works on it last; the pieces of
+// its other k blocks were produced FIRST by the following CTAs, which drop
+// them (fp32) into their workspace slot and publish `epoch`.  The owner adds
+// them in k order after its own partial (deterministic) and runs the fused
+// epilogue, so the reduction never stalls the weight stream.
+struct StreamK {
+  float* ws;             // [grid][NT * BM] fp32 pieces
+  std::int32_t* flags;   // [grid] epoch of the piece in the slot
+  std::int32_t epoch;
+};
+
+__device__ __forceinline__ int sk_cta_of(long long u, long long total, int G) {
+  // the CTA whose range [c*total/G, (c+1)*total/G) holds unit u
+  int c = static_cast<int>(u * G / total);
+  while (c + 1 < G && (static_cast<long long>(c + 1) * total) / G <= u) ++c;
+  while (c > 0 && (static_cast<long long>(c) * total) / G > u) --c;
+  return c;
+}
+
 template <int NT, int STAGES>
 __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant__ CUtensorMap map_w,
                                                            const __grid_constant__ CUtensorMap map_a, GemmArgs args,
-                                                           int S) {
+                                                           int S, StreamK sk) {
   using L = SkSmem<NT, STAGES>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -225,6 +249,24 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   const int t0 = static_cast<int>(static_cast<long long>(cid) * tiles / n_clusters);
   const int t1 = static_cast<int>(static_cast<long long>(cid + 1) * tiles / n_clusters);
   const int kb0 = rank * kblocks / S, kb1 = (rank + 1) * kblocks / S;
+  // Segments of this CTA: (tile, [kb_a, kb_b)).  Cluster split-K / whole
+  // tiles: t0..t1 with [kb0, kb1).  Stream-K: the unit range [u0, u1).
+  const bool streamk = sk.ws != nullptr;
+  const long long total_u = static_cast<long long>(tiles) * kblocks;
+  const long long u0 = streamk ? static_cast<long long>(blockIdx.x) * total_u / gridDim.x : 0;
+  const long long u1 = streamk ? static_cast<long long>(blockIdx.x + 1) * total_u / gridDim.x : 0;
+  const int seg_first_t = streamk ? static_cast<int>(u0 / kblocks) : t0;
+  const int seg_end_t = streamk ? (u1 > u0 ? static_cast<int>((u1 - 1) / kblocks) + 1 : seg_first_t) : t1;
+  auto seg_kb = [&](int t, int& a, int& b) {
+    if (!streamk) {
+      a = kb0;
+      b = kb1;
+      return;
+    }
+    const long long lo = static_cast<long long>(t) * kblocks, hi = lo + kblocks;
+    a = static_cast<int>((u0 > lo ? u0 : lo) - lo);
+    b = static_cast<int>((u1 < hi ? u1 : hi) - lo);
+  };
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_w)) : "memory");
@@ -260,24 +302,35 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
       // Weights do not depend on the predecessor kernel: the first ring's
       // worth of weight tiles streams in while it is still finishing; the
       // activation tiles follow griddepcontrol.wait.
-      const int per_tile = kb1 - kb0, total = (t1 - t0) * per_tile;
-      const int early = args.no_early_w ? 0 : (total < STAGES ? total : STAGES);
-      for (int i = 0; i < early; ++i) {
-        const int t = t0 + i / per_tile, kb = kb0 + i % per_tile;
-        mbar_expect_tx(&full[i], L::STAGE_BYTES);
-        tma_load_2d(smem + i * L::STAGE_BYTES, &map_w, &full[i], 0, (t * kblocks + kb) * BM);
+      int early_kb[STAGES];
+      int early = 0;
+      if (!args.no_early_w) {
+        for (int t = seg_first_t; t < seg_end_t && early < STAGES; ++t) {
+          int a, b;
+          seg_kb(t, a, b);
+          for (int kb = a; kb < b && early < STAGES; ++kb, ++early) {
+            early_kb[early] = kb;
+            mbar_expect_tx(&full[early], L::STAGE_BYTES);
+            tma_load_2d(smem + early * L::STAGE_BYTES, &map_w, &full[early], 0, (t * kblocks + kb) * BM);
+          }
+        }
       }
       pdl_wait();
       for (int i = 0; i < early; ++i)
-        tma_load_2d(smem + i * L::STAGE_BYTES + L::A_BYTES, &map_a, &full[i], (kb0 + i % per_tile) * BK, 0);
-      for (int i = early; i < total; ++i) {
-        const int t = t0 + i / per_tile, kb = kb0 + i % per_tile;
-        const int st = i % STAGES;
-        mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
-        unsigned char* sw = smem + st * L::STAGE_BYTES;
-        mbar_expect_tx(&full[st], L::STAGE_BYTES);
-        tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
-        tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
+        tma_load_2d(smem + i * L::STAGE_BYTES + L::A_BYTES, &map_a, &full[i], early_kb[i] * BK, 0);
+      int i = 0;
+      for (int t = seg_first_t; t < seg_end_t; ++t) {
+        int a, b;
+        seg_kb(t, a, b);
+        for (int kb = a; kb < b; ++kb, ++i) {
+          if (i < early) continue;
+          const int st = i % STAGES;
+          mbar_wait(&empty[st], ((i / STAGES) - 1) & 1);
+          unsigned char* sw = smem + st * L::STAGE_BYTES;
+          mbar_expect_tx(&full[st], L::STAGE_BYTES);
+          tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
+          tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -285,12 +338,14 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
       constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(NT >> 3) << 17) |
                                       (static_cast<std::uint32_t>(BM >> 4) << 24);
       int i = 0;
-      for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+      for (int t = seg_first_t, seg = 0; t < seg_end_t; ++t, ++seg) {
         const int buf = seg & 1;
+        int ka, kbe;
+        seg_kb(t, ka, kbe);
         if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const std::uint32_t acc_tmem = tmem + buf * NT;
-        for (int kb = kb0; kb < kb1; ++kb, ++i) {
+        for (int kb = ka; kb < kbe; ++kb, ++i) {
           const int st = i % STAGES;
           mbar_wait(&full[st], (i / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -298,7 +353,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
           const std::uint64_t da = smem_desc(sw), db = smem_desc(sw + L::A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
-            const std::uint32_t acc = (kb > kb0 || k > 0) ? 1u : 0u;
+            const std::uint32_t acc = (kb > ka || k > 0) ? 1u : 0u;
             asm volatile(
                 "{\n"
                 ".reg .pred p;\n"
@@ -321,11 +376,66 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
     const int q = warp - 4, row = q * 32 + lane;
     const int mcols = min(args.M, NT);
     const int m_lo = rank * mcols / S, m_hi = (rank + 1) * mcols / S;
-    for (int t = t0, seg = 0; t < t1; ++t, ++seg) {
+    for (int t = seg_first_t, seg = 0; t < seg_end_t; ++t, ++seg) {
       const int buf = seg & 1;
       const int n = t * BM + row;
       mbar_wait(&tfull[buf], (seg / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (streamk) {
+        int ka, kbe;
+        seg_kb(t, ka, kbe);
+        float* mine = sk.ws + static_cast<std::int64_t>(blockIdx.x) * (NT * BM);
+        if (ka > 0) {
+          // A piece (end / middle of a tile owned by an earlier CTA): fp32 -> slot, then publish.
+#pragma unroll 1
+          for (int cc = 0; cc < mcols; cc += 16) {
+            std::uint32_t r[16];
+            tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + cc, r);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) mine[(cc + j) * BM + row] = __uint_as_float(r[j]);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __threadfence();
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the 4 epilogue warps
+          if (q == 0 && lane == 0)
+            asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(sk.flags + blockIdx.x), "r"(sk.epoch) : "memory");
+        } else {
+          // Whole tile, or the owner of a tile whose later k blocks are pieces of the next CTAs.
+          const int c_last = kbe < kblocks ? sk_cta_of(static_cast<long long>(t + 1) * kblocks - 1, total_u, gridDim.x)
+                                           : static_cast<int>(blockIdx.x);
+          for (int p = blockIdx.x + 1; p <= c_last; ++p) {
+            const long long t_start = clock64();
+            while (true) {
+              std::int32_t e;
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + p) : "memory");
+              if (e == sk.epoch) break;
+              if (clock64() - t_start > kWaitLimitCycles) {
+                printf("ib2 watchdog: stream-K piece of CTA %d (epoch %d) missing for CTA %d\n", p, sk.epoch,
+                       blockIdx.x);
+                __trap();
+              }
+            }
+          }
+#pragma unroll 1
+          for (int cc = 0; cc < mcols; cc += 16) {
+            std::uint32_t r[16];
+            tmem_ld16(tmem + buf * NT + (static_cast<std::uint32_t>(q * 32) << 16) + cc, r);
+            float v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+            for (int p = blockIdx.x + 1; p <= c_last; ++p) {
+              const float* piece = sk.ws + static_cast<std::int64_t>(p) * (NT * BM);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] += __ldcg(piece + (cc + j) * BM + row);
+            }
+            epi_rows16(args, n, cc, v, lane);
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[buf])) : "memory");
+        continue;
+      }
       constexpr int NS = L::PART_SLOTS > 0 ? L::PART_SLOTS : 1;
       const int slot = seg % NS;
       float* part = parts + slot * (NT * BM);
@@ -859,6 +969,27 @@ SplitPlan plan_split(Kernel kernel, int smem, int tiles, int kblocks, bool split
   return {S, tiles};
 }
 
+// Stream-K workspace, one per stream (GEMMs on different streams may run
+// concurrently): a piece slot per CTA + its epoch flag.
+StreamK streamk_for(cudaStream_t s) {
+  struct Ws {
+    float* ws = nullptr;
+    std::int32_t* flags = nullptr;
+    std::int32_t epoch = 0;
+  };
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, Ws> pool;
+  std::lock_guard<std::mutex> g(mu);
+  Ws& w = pool[s];
+  if (!w.ws) {
+    IB2_CUDA(cudaMalloc(&w.ws, static_cast<std::size_t>(g_sms) * 256 * BM * sizeof(float)));
+    IB2_CUDA(cudaMalloc(&w.flags, static_cast<std::size_t>(g_sms) * sizeof(std::int32_t)));
+    IB2_CUDA(cudaMemset(w.flags, 0, static_cast<std::size_t>(g_sms) * sizeof(std::int32_t)));
+  }
+  w.epoch = w.epoch == 0x7fffffff ? 1 : w.epoch + 1;
+  return StreamK{w.ws, w.flags, w.epoch};
+}
+
 template <int NT, int STAGES>
 void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   using L = SkSmem<NT, STAGES>;
@@ -874,7 +1005,20 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   if (force_s > 0 && L::SPLIT_OK)
     sp = {force_s, std::max(1, std::min(max_clusters(tc_splitk_kernel<NT, STAGES>, force_s, L::TOTAL), tiles))};
   static const bool verbose = getenv("IB2_SPLIT_VERBOSE") != nullptr;
-  if (verbose) fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d\n", a.N, a.K, a.M, sp.S, sp.clusters);
+  // Whole tiles that do not fill the SMs evenly: stream-K over every SM.
+  static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
+  // Owners spin on pieces of later CTAs, so two stream-K GEMMs must never run
+  // concurrently (each could hold SMs the other's pieces need): the executor
+  // allows it on its compute stream only.
+  const bool use_sk = a.streamk_ok && sp.S == 1 && !no_streamk && tiles % g_sms != 0 && kblocks >= 2;
+  StreamK sk{nullptr, nullptr, 0};
+  if (use_sk) {
+    sk = streamk_for(s);
+    sp.clusters = std::min<long long>(g_sms, static_cast<long long>(tiles) * kblocks);
+  }
+  if (verbose)
+    fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d%s\n", a.N, a.K, a.M, sp.S, sp.clusters,
+            use_sk ? " stream-K" : "");
   const std::int64_t a_rows = a.a_rows > 0 ? a.a_rows : (g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
@@ -892,7 +1036,7 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_splitk_kernel<NT, STAGES>, mw, ma, a, sp.S));
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_splitk_kernel<NT, STAGES>, mw, ma, a, sp.S, sk));
 }
 
 bool skinny_ok(const GemmArgs& a) {
@@ -981,6 +1125,7 @@ void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, cons
                 void* outf, int ldf, int flags, void* stream) {
   const bool force_simt = flags & 1;
   g_force_pair_bn = (flags & 4) ? 128 : (flags & 8) ? 256 : 0;
+  const int streamk_ok = (flags & 16) ? 0 : 1;
   if (!(flags & 2)) {
   // The executor keeps weights tile-blocked; the hook takes row-major W.
   static f16* tiled = nullptr;
@@ -996,6 +1141,7 @@ void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, cons
   }
   GemmArgs g{static_cast<const f16*>(a), static_cast<const f16*>(w), M, N, K, static_cast<Epi>(epi),
              static_cast<const f16*>(bias), static_cast<f16*>(out), ldo, static_cast<float*>(outf), ldf};
+  g.streamk_ok = streamk_ok;
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const std::int64_t saved = g_a_rows_capacity;
   g_a_rows_capacity = 0;  // caller buffers are exactly M rows

@@ -114,6 +114,24 @@ def test_pair_gemm_tile_widths(M, N, K, epi, flags):
     _check(M, N, K, epi, flags)
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(32, 12288, 4096, STORE), (29, 50400, 4096, STOREF32), (45, 16384, 4096, GELU),
+                                       (200, 16384, 4096, SWIGLU), (16, 4096, 16384, RESID), (1, 256, 256, STORE),
+                                       (250, 4096, 4096, RESID)])
+def test_decode_gemm_stream_k(M, N, K, epi):
+    """Stream-K (whole-tile decode GEMMs over every SM) against the fp32
+    reference, the classic tile split (flag 16) and itself (deterministic)."""
+    import torch
+    _check(M, N, K, epi)
+    _check(M, N, K, epi, flags=16)
+    torch.manual_seed(1)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
+    resid = torch.randn(M, N, device="cuda") if epi == RESID else None
+    x = run_gemm(a, w, epi, None, resid).clone()
+    y = run_gemm(a, w, epi, None, resid).clone()
+    assert torch.equal(x, y), "stream-K result not deterministic"
+
+
 @pytest.mark.parametrize("M,N,K", [(77, 1024, 1024), (640, 4096, 4096)])
 def test_tcgen05_matches_simt(M, N, K):
     import torch
