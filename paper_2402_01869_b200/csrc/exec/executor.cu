@@ -1029,6 +1029,16 @@ void Impl::consume(const isim_batch_plan& p) {
         combines.back().nparts += 1;
       }
     }
+    // Longest items first (LPT): the CTAs are issued in item order, and a
+    // causal prompt's last query tiles see 10-30x the keys of its first ones;
+    // issued last, they set the kernel's tail (C3 recompute chunks: a 2,048-row
+    // item list is 1..16 key units per item over 296 CTA slots).  Items carry
+    // their rows, keys and partial slot, so the order is free.
+    std::stable_sort(items.begin(), items.end(), [](const TileDesc& a, const TileDesc& b) {
+      const int ka = std::min(a.kv_hi, a.pos0 + a.nrows) - a.kv_lo;
+      const int kb = std::min(b.kv_hi, b.pos0 + b.nrows) - b.kv_lo;
+      return ka > kb;
+    });
   }
 
   std::vector<std::int64_t> sw_in_req;

@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kK2Threads, AttnCfg<HD>::CTAS) chunk_attn_tc_k
   std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(pvdone + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y;
+  const int h = blockIdx.x;  // heads fastest: CTAs issue item by item (items are longest first)
   if (threadIdx.x == 0 && smem - smem_raw > C::SLACK) __trap();  // layout would overrun the allocation
 
   if (warp == 0 && lane == 0) {
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(kK2Threads, AttnCfg<HD>::CTAS) chunk_attn_tc_k
   items = after_wait(items);
   table = after_wait(table);
 
-  const TileDesc td = items[blockIdx.x];
+  const TileDesc td = items[blockIdx.y];
   const int last_pos = td.pos0 + td.nrows - 1;
   const int kv_hi = min(td.kv_hi, last_pos + 1);
   const int kt0 = td.kv_lo / BN;
@@ -454,7 +454,8 @@ void launch_chunk_hd(const f16* qkv, int qkv_rows, const TileDesc* items, int n_
     configured = true;
   }
   const std::int64_t layer_row0 = static_cast<std::int64_t>(layer) * g.num_blocks * 2 * g.heads * kBlockTokens;
-  launch_pdl(chunk_attn_tc_kernel<HD>, dim3(n_items, g.heads), dim3(kK2Threads), C::TOTAL, s, q_map(qkv, qkv_rows, g.heads * HD),
+  if (n_items > 65535) throw DeviceError("chunk attention: too many work items");
+  launch_pdl(chunk_attn_tc_kernel<HD>, dim3(g.heads, n_items), dim3(kK2Threads), C::TOTAL, s, q_map(qkv, qkv_rows, g.heads * HD),
              kv_map(g), items, g.table, g.max_lblocks, layer_row0, g.heads, out, ws_o, ws_ml);
   IB2_LAUNCH_CHECK();
 }
