@@ -466,6 +466,37 @@ def cpu_full_trace_seconds(preset, plans):
         return (time.perf_counter() - t) / len(plans)
 
 
+def validate_depth(preset, layers_total, plans):
+    """Check the layer extrapolation on the sampled plan with the least KV:
+    its 1- and 2-layer forwards extrapolated to `layers_total` vs the same
+    plan run at full depth (memory: the oracle keeps fp32 KV of every layer)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle.forward import ForwardOracle
+
+    def kv_of(pj):
+        return sum(pos + count for (rid, pos, count, kind, sample) in pj["spans"])
+    pj = min(plans, key=kv_of)
+    out = {"iteration": pj["it"], "rows": sum(sp[2] for sp in pj["spans"]), "keys": kv_of(pj)}
+    with threadpool_limits(limits=os.cpu_count()):
+        for layers in (1, 2, layers_total):
+            fo = ForwardOracle({"preset": preset, "layers": layers, "max_pos": 4160}, fast_random=True,
+                               precision="f32")
+            for (rid, pos, count, kind, sample) in pj["spans"]:
+                fo._ensure(rid, pos + count + 1)
+            for kv in fo.kv.values():
+                kv.fill(np.float32(1e-3))
+            fo._forward_only(pj)
+            t = time.perf_counter()
+            fo._forward_only(pj)
+            out[f"t{layers}"] = time.perf_counter() - t
+            del fo
+    out["extrapolated"] = out["t1"] + (layers_total - 1) * (out["t2"] - out["t1"])
+    out["measured"] = out[f"t{layers_total}"]
+    out["measured_over_extrapolated"] = out["measured"] / out["extrapolated"]
+    return out
+
+
 def cpu_reference(cfg, args, wins):
     """The reference's CPU path on this host (see module docstring)."""
     from oracle.ref_plans import reference_schedule, run_reference as ref_run
@@ -486,6 +517,8 @@ def cpu_reference(cfg, args, wins):
                            f"from the reference's event log): {per_iter * 1e3:.2f} ms/iteration, measured over the "
                            f"whole trace")}
     per_iter, det = cpu_forward_seconds(cfg["model"]["preset"], cfg["layers"], plans)
+    if getattr(args, "validate_depth", False):
+        det["depth_check"] = validate_depth(cfg["model"]["preset"], cfg["layers"], plans)
     per_iter += t_sched
     value = summ["done_events"] / (summ["iterations"] * per_iter)
     return {"value": value, "s_per_iteration": per_iter, "cores": det["cores"], "iterations": summ["iterations"],
@@ -524,6 +557,7 @@ def run_reference(args):
         "cpu_baseline": {"value": v, "unit": "req/s", "cores": cpu["cores"], "kind": "port",
                          "sample": cpu["sample"]},
         "forward_runs_s": cpu["forward"]["runs"],
+        "depth_check": cpu["forward"].get("depth_check"),
         "e2e": {"value": v, "unit": "req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -539,6 +573,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--host-gb", type=float, default=0.0, help="pinned host pool per rank (default: ledger x 1.25)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--validate-depth", action="store_true",
+                    help="CPU path: also run the smallest sampled iteration at full depth to check the extrapolation")
     ap.add_argument("--full-trace", action="store_true",
                     help="CPU path: time the oracle forward over every iteration (C0 only: minutes)")
     ap.add_argument("--gpu-blocks", type=int, default=0,

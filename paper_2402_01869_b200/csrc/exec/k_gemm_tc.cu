@@ -646,10 +646,64 @@ __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, flo
   }
 }
 
+// Work of one CTA pair: whole tiles in data-parallel rounds (t = pair,
+// pair + npairs, ...) while every pair has one, then -- stream-K tail (sk.ws
+// set) -- the remaining T mod npairs tiles' (tile, k block) units split
+// evenly over all pairs, so no pair idles through a last partial round.
+// Segment = (tile, [a, b)) of k blocks; a tail tile's pieces (a > 0) are
+// produced at the start of the later pairs' tails, its owner (a == 0) ends
+// its own tail with it and adds the pieces in k order (deterministic).
+struct PairSegs {
+  int pair, npairs, total, nk, dp_tiles, rem;
+  long long u0, u1;  // this pair's tail units
+  int t, a, b;       // current segment
+  int dp_next;
+  long long u;
+  __device__ void init(int p, int np, int tot, int nkb, bool streamk) {
+    pair = p;
+    npairs = np;
+    total = tot;
+    nk = nkb;
+    dp_tiles = streamk ? (tot / np) * np : tot;
+    rem = tot - dp_tiles;
+    const long long units = static_cast<long long>(rem) * nk;
+    u0 = units * p / np;
+    u1 = units * (p + 1) / np;
+    dp_next = p;
+    u = u0;
+  }
+  __device__ bool next() {
+    if (dp_next < dp_tiles) {
+      t = dp_next;
+      a = 0;
+      b = nk;
+      dp_next += npairs;
+      return true;
+    }
+    if (u >= u1) return false;
+    const int tl = static_cast<int>(u / nk);
+    t = dp_tiles + tl;
+    a = static_cast<int>(u - static_cast<long long>(tl) * nk);
+    const long long end = static_cast<long long>(tl + 1) * nk;
+    b = static_cast<int>((u1 < end ? u1 : end) - static_cast<long long>(tl) * nk);
+    u = static_cast<long long>(tl) * nk + b;
+    return true;
+  }
+  // last pair whose tail holds a unit of tail tile t (t >= dp_tiles)
+  __device__ int last_pair_of(int tile) const {
+    const long long units = static_cast<long long>(rem) * nk;
+    const long long uu = static_cast<long long>(tile - dp_tiles + 1) * nk - 1;
+    int c = static_cast<int>(uu * npairs / units);
+    while (c + 1 < npairs && units * (c + 1) / npairs <= uu) ++c;
+    while (c > 0 && units * c / npairs > uu) --c;
+    return c;
+  }
+};
+
 template <int BN>
 __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                                                               const __grid_constant__ CUtensorMap map_w,
-                                                              GemmArgs args) {
+                                                              GemmArgs args, StreamK sk) {
   using L = PairSmem<BN>;
   constexpr int STAGES = L::STAGES;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -667,6 +721,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
   const int MT = (args.M + 255) / 256, NTL = (args.N + BN - 1) / BN;
   const int total = MT * NTL;
   const int nk = args.K / BK;
+  const bool streamk = sk.ws != nullptr;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_a)) : "memory");
@@ -710,18 +765,22 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
         return BN == 256 ? ((ntl * 2 + static_cast<int>(rank)) * nk + kb) * 128
                          : (ntl * nk + kb) * 128 + static_cast<int>(rank) * 64;
       };
-      for (int t = pair; t < total && pre < STAGES && !args.no_early_w; t += npairs) {
-        for (int kb = 0; kb < nk && pre < STAGES; ++kb, ++pre) {
+      PairSegs it;
+      it.init(pair, npairs, total, nk, streamk);
+      while (pre < STAGES && !args.no_early_w && it.next()) {
+        for (int kb = it.a; kb < it.b && pre < STAGES; ++kb, ++pre) {
           if (leader) mbar_expect_tx(&full[pre], 2 * L::STAGE_BYTES);
-          tma_load_2d_pair(smem + pre * L::STAGE_BYTES + L::A_BYTES, &map_w, full0 + pre * 8, 0, wrow(t / MT, kb));
+          tma_load_2d_pair(smem + pre * L::STAGE_BYTES + L::A_BYTES, &map_w, full0 + pre * 8, 0, wrow(it.t / MT, kb));
         }
       }
       pdl_wait();
       int i = 0;
-      for (int t = pair; t < total; t += npairs) {
+      it.init(pair, npairs, total, nk, streamk);
+      while (it.next()) {
+        const int t = it.t;
         const int mt = t % MT, ntl = t / MT;
         const int arow = mt * 256 + static_cast<int>(rank) * 128;
-        for (int kb = 0; kb < nk; ++kb, ++i) {
+        for (int kb = it.a; kb < it.b; ++kb, ++i) {
           const int st = i % STAGES;
           unsigned char* sa = smem + st * L::STAGE_BYTES;
           const std::uint32_t bar = full0 + st * 8;
@@ -741,12 +800,15 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       constexpr std::uint32_t idesc = (1u << 4) | (static_cast<std::uint32_t>(BN >> 3) << 17) |
                                       (static_cast<std::uint32_t>(256 >> 4) << 24);
       int i = 0, seg = 0;
-      for (int t = pair; t < total; t += npairs, ++seg) {
+      PairSegs it;
+      it.init(pair, npairs, total, nk, streamk);
+      for (; it.next(); ++seg) {
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], ((seg / 2) - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const std::uint32_t acc_tmem = tmem + buf * BN;
-        for (int kb = 0; kb < nk; ++kb, ++i) {
+        const int ka = it.a;
+        for (int kb = it.a; kb < it.b; ++kb, ++i) {
           const int st = i % STAGES;
           mbar_wait(&full[st], (i / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -754,7 +816,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
           const std::uint64_t da = smem_desc(sa), db = smem_desc(sa + L::A_BYTES);
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
-            const std::uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            const std::uint32_t acc = (kb > ka || k > 0) ? 1u : 0u;
             asm volatile(
                 "{\n"
                 ".reg .pred p;\n"
@@ -781,20 +843,73 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
     const int q = warp - 4;
     const std::uint32_t tempty0 = mapa_rank(su32(tempty), 0);
     int seg = 0;
-    for (int t = pair; t < total; t += npairs, ++seg) {
+    PairSegs it;
+    it.init(pair, npairs, total, nk, streamk);
+    const int row = q * 32 + lane;  // this thread's row of the CTA's 128
+    for (; it.next(); ++seg) {
+      const int t = it.t;
       const int buf = seg & 1;
       const int mt = t % MT, ntl = t / MT;
-      const int m = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+      const int m = mt * 256 + static_cast<int>(rank) * 128 + row;
       mbar_wait(&tfull[buf], (seg / 2) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (it.a > 0) {
+        // A piece of a tail tile owned by an earlier pair: fp32 -> this CTA's slot, publish.
+        float* mine = sk.ws + static_cast<std::int64_t>(blockIdx.x) * (128 * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        std::uint32_t r[16];
-        tmem_ld16(tmem + buf * BN + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
-        float v[16];
+        for (int c = 0; c < BN; c += 16) {
+          std::uint32_t r[16];
+          tmem_ld16(tmem + buf * BN + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
+          float4* d4 = reinterpret_cast<float4*>(mine + static_cast<std::int64_t>(row) * BN + c);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        epi_cols16(args, m, ntl * BN + c, v);
+          for (int j = 0; j < 4; ++j)
+            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                                __uint_as_float(r[4 * j + 3]));
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __threadfence();
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // this CTA's 4 epilogue warps
+        if (q == 0 && lane == 0)
+          asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(sk.flags + blockIdx.x), "r"(sk.epoch) : "memory");
+      } else {
+        // Whole tile, or owner of a tail tile: wait for the later pairs' pieces.
+        const int p_last = it.b < nk ? it.last_pair_of(t) : pair;
+        for (int pp = pair + 1; pp <= p_last; ++pp) {
+          const int cta = 2 * pp + static_cast<int>(rank);
+          const long long t_start = clock64();
+          while (true) {
+            std::int32_t e;
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + cta) : "memory");
+            if (e == sk.epoch) break;
+            if (clock64() - t_start > kWaitLimitCycles) {
+              printf("ib2 watchdog: pair stream-K piece of CTA %d (epoch %d) missing for CTA %d\n", cta, sk.epoch,
+                     blockIdx.x);
+              __trap();
+            }
+          }
+        }
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+          std::uint32_t r[16];
+          tmem_ld16(tmem + buf * BN + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          for (int pp = pair + 1; pp <= p_last; ++pp) {
+            const float4* s4 = reinterpret_cast<const float4*>(
+                sk.ws + static_cast<std::int64_t>(2 * pp + static_cast<int>(rank)) * (128 * BN) +
+                static_cast<std::int64_t>(row) * BN + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 x = __ldcg(s4 + j);
+              v[4 * j] += x.x;
+              v[4 * j + 1] += x.y;
+              v[4 * j + 2] += x.z;
+              v[4 * j + 3] += x.w;
+            }
+          }
+          epi_cols16(args, m, ntl * BN + c, v);
+        }
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncwarp();
@@ -876,6 +991,8 @@ std::int64_t g_a_rows_capacity = 0;  // rows of every activation buffer (set by 
 
 int g_sms = 0;
 
+StreamK streamk_for(cudaStream_t s);
+
 template <int BN>
 void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   using L = PairSmem<BN>;
@@ -888,7 +1005,12 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, 128);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN / 2);
   const int tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
-  const int pairs = std::max(1, std::min(g_sms / 2, tiles));
+  // Tiles that do not divide into whole rounds over the pairs: stream-K tail
+  // over every pair (compute stream only, see StreamK).
+  static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
+  const bool use_sk = a.streamk_ok && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
+  const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
+  const int pairs = use_sk ? g_sms / 2 : std::max(1, std::min(g_sms / 2, tiles));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(256);
@@ -903,7 +1025,7 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN>, ma, mw, a));
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<BN>, ma, mw, a, sk));
 }
 
 int g_force_pair_bn = 0;  // isim_debug_gemm flags 4 / 8: force the 128 / 256 tile width

@@ -132,6 +132,24 @@ def test_decode_gemm_stream_k(M, N, K, epi):
     assert torch.equal(x, y), "stream-K result not deterministic"
 
 
+@pytest.mark.parametrize("M,N,K,epi", [(1218, 5120, 5120, RESID), (300, 1000, 512, GELU), (2065, 15360, 5120, STORE),
+                                       (513, 27648, 5120, SWIGLU), (1218, 5120, 13824, RESID), (257, 4096, 4096, STOREF32)])
+def test_pair_gemm_stream_k_tail(M, N, K, epi):
+    """CTA-pair GEMM with the stream-K tail (tiles not a multiple of the 74
+    pairs) against the fp32 reference, without the tail (flag 16), and itself
+    (deterministic)."""
+    import torch
+    _check(M, N, K, epi)
+    _check(M, N, K, epi, flags=16)
+    torch.manual_seed(2)
+    a = (torch.randn(M, K, device="cuda") * 0.5).half()
+    w = (torch.randn(N, K, device="cuda") * 0.02).half()
+    resid = torch.randn(M, N, device="cuda") if epi == RESID else None
+    x = run_gemm(a, w, epi, None, resid).clone()
+    y = run_gemm(a, w, epi, None, resid).clone()
+    assert torch.equal(x, y), "stream-K tail result not deterministic"
+
+
 @pytest.mark.parametrize("M,N,K", [(77, 1024, 1024), (640, 4096, 4096)])
 def test_tcgen05_matches_simt(M, N, K):
     import torch
