@@ -647,30 +647,32 @@ __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, flo
 }
 
 // Work of one CTA pair: whole tiles in data-parallel rounds (t = pair,
-// pair + npairs, ...) while every pair has one, then -- stream-K tail (sk.ws
-// set) -- the remaining T mod npairs tiles' (tile, k block) units split
-// evenly over all pairs, so no pair idles through a last partial round.
-// Segment = (tile, [a, b)) of k blocks; a tail tile's pieces (a > 0) are
-// produced at the start of the later pairs' tails, its owner (a == 0) ends
-// its own tail with it and adds the pieces in k order (deterministic).
+// pair + npairs, ...) while every pair has one, then -- split tail (sk.ws
+// set) -- each of the remaining T mod npairs tiles is shared by a group of g
+// = min(4, npairs / rem) pairs, each taking 1/g of its k blocks, instead of
+// one pair per tile while the rest idle through a last partial round.  The
+// group's first pair owns the tile: it waits for the other g - 1 fp32
+// pieces (computed at the same time) and adds them in k order
+// (deterministic).  (Spreading a tail tile over every pair, classic
+// stream-K, measured slower: the owner's read of ~17 pieces outweighed the
+// saved k blocks.)
 struct PairSegs {
-  int pair, npairs, total, nk, dp_tiles, rem;
-  long long u0, u1;  // this pair's tail units
-  int t, a, b;       // current segment
+  int pair, npairs, total, nk, dp_tiles, rem, g;
+  int t, a, b;  // current segment
   int dp_next;
-  long long u;
-  __device__ void init(int p, int np, int tot, int nkb, bool streamk) {
+  bool tail_done;
+  __device__ void init(int p, int np, int tot, int nkb, bool split_tail) {
     pair = p;
     npairs = np;
     total = tot;
     nk = nkb;
-    dp_tiles = streamk ? (tot / np) * np : tot;
+    dp_tiles = split_tail ? (tot / np) * np : tot;
     rem = tot - dp_tiles;
-    const long long units = static_cast<long long>(rem) * nk;
-    u0 = units * p / np;
-    u1 = units * (p + 1) / np;
+    g = rem > 0 ? np / rem : 1;
+    g = g < 1 ? 1 : (g > 4 ? 4 : g);
+    g = g > nk ? nk : g;
     dp_next = p;
-    u = u0;
+    tail_done = false;
   }
   __device__ bool next() {
     if (dp_next < dp_tiles) {
@@ -680,24 +682,17 @@ struct PairSegs {
       dp_next += npairs;
       return true;
     }
-    if (u >= u1) return false;
-    const int tl = static_cast<int>(u / nk);
-    t = dp_tiles + tl;
-    a = static_cast<int>(u - static_cast<long long>(tl) * nk);
-    const long long end = static_cast<long long>(tl + 1) * nk;
-    b = static_cast<int>((u1 < end ? u1 : end) - static_cast<long long>(tl) * nk);
-    u = static_cast<long long>(tl) * nk + b;
+    if (tail_done) return false;
+    tail_done = true;
+    if (pair >= rem * g) return false;
+    const int part = pair % g;
+    t = dp_tiles + pair / g;
+    a = part * nk / g;
+    b = (part + 1) * nk / g;
     return true;
   }
-  // last pair whose tail holds a unit of tail tile t (t >= dp_tiles)
-  __device__ int last_pair_of(int tile) const {
-    const long long units = static_cast<long long>(rem) * nk;
-    const long long uu = static_cast<long long>(tile - dp_tiles + 1) * nk - 1;
-    int c = static_cast<int>(uu * npairs / units);
-    while (c + 1 < npairs && units * (c + 1) / npairs <= uu) ++c;
-    while (c > 0 && units * c / npairs > uu) --c;
-    return c;
-  }
+  // pairs holding the later k parts of this pair's tail tile (owner only)
+  __device__ int last_pair_of(int) const { return (pair / g) * g + g - 1; }
 };
 
 template <int BN>
@@ -873,7 +868,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
           asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(sk.flags + blockIdx.x), "r"(sk.epoch) : "memory");
       } else {
         // Whole tile, or owner of a tail tile: wait for the later pairs' pieces.
-        const int p_last = it.b < nk ? it.last_pair_of(t) : pair;
+        const int p_last = it.b < nk ? it.last_pair_of(t) : pair;  // a < b < nk only for a split tail owner
         for (int pp = pair + 1; pp <= p_last; ++pp) {
           const int cta = 2 * pp + static_cast<int>(rank);
           const long long t_start = clock64();
@@ -1005,8 +1000,8 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, 128);
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BN / 2);
   const int tiles = ((a.M + 255) / 256) * ((a.N + BN - 1) / BN);
-  // Tiles that do not divide into whole rounds over the pairs: stream-K tail
-  // over every pair (compute stream only, see StreamK).
+  // Tiles that do not divide into whole rounds over the pairs: split tail
+  // (PairSegs; compute stream only, see StreamK).
   static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
   const bool use_sk = a.streamk_ok && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
   const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
