@@ -200,8 +200,9 @@ void isim_session_free(isim_session* s);
  * add (+bias), 3 SwiGLU pairs -> fp16 [M][N/2], 4 store fp32 (+bias)).
  * flags bit 0: run the CUDA-core kernel instead of tcgen05; bit 1: W is
  * already tile-blocked (isim_debug_tile_weights), else row-major; bit 2 / 3:
- * force the 256x128 / 256x256 tile of the M > 256 kernel; bit 4: no stream-K
- * in the M <= 256 kernel.  Asynchronous on `stream` (may be 0). */
+ * force the 256x128 / 256x256 tile of the M > 256 kernel; bit 4: no stream-K /
+ * split tail; bit 5: force them (default: IB2_STREAMK=1 enables them).
+ * Asynchronous on `stream` (may be 0). */
 isim_status isim_debug_gemm(const void* a, const void* w, int32_t M, int32_t N, int32_t K, int32_t epi,
                             const void* bias, void* out, int32_t ldo, void* outf, int32_t ldf, int32_t flags,
                             void* stream);

@@ -158,7 +158,8 @@ struct GemmArgs {
   int no_early_w;      // diagnostics: no weight prefetch before griddepcontrol.wait
   const float* addf;   // Epi::ResidAdd: if set, outf = (outf + acc) + addf (same [M][ldf] layout)
   std::int64_t a_rows;  // rows addressable from `a` for TMA bounds (0: the executor's buffer capacity)
-  int streamk_ok;       // decode GEMM may use stream-K (only where no other stream-K GEMM runs concurrently)
+  int streamk_ok;       // 0: no stream-K / split tail; 1: if enabled (IB2_STREAMK=1); 2: forced.  Only where no
+                        // other stream-K GEMM can run concurrently (the executor's compute stream)
 };
 
 }  // namespace ib2

@@ -988,6 +988,12 @@ int g_sms = 0;
 
 StreamK streamk_for(cudaStream_t s);
 
+// GemmArgs::streamk_ok: 0 never, 1 if enabled (IB2_STREAMK=1), 2 forced (tests).
+bool streamk_enabled(const GemmArgs& a) {
+  static const bool env_on = getenv("IB2_STREAMK") != nullptr;
+  return a.streamk_ok == 2 || (a.streamk_ok == 1 && env_on);
+}
+
 template <int BN>
 void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   using L = PairSmem<BN>;
@@ -1003,7 +1009,7 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   // Tiles that do not divide into whole rounds over the pairs: split tail
   // (PairSegs; compute stream only, see StreamK).
   static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
-  const bool use_sk = a.streamk_ok && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
+  const bool use_sk = streamk_enabled(a) && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
   const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
   const int pairs = use_sk ? g_sms / 2 : std::max(1, std::min(g_sms / 2, tiles));
   cudaLaunchConfig_t cfg{};
@@ -1126,8 +1132,11 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
   // Owners spin on pieces of later CTAs, so two stream-K GEMMs must never run
   // concurrently (each could hold SMs the other's pieces need): the executor
-  // allows it on its compute stream only.
-  const bool use_sk = a.streamk_ok && sp.S == 1 && !no_streamk && tiles % g_sms != 0 && kblocks >= 2;
+  // allows it on its compute stream only.  Opt-in (streamk_enabled): measured
+  // per GEMM (profiles/r2o/streamk_per_gemm.txt) it wins on a few shapes
+  // (GPT-J QKV at M = 32: +9 %) and loses on more (M = 108: -14..-26 %), and
+  // C4 end to end ran 2.3 % slower with it.
+  const bool use_sk = streamk_enabled(a) && sp.S == 1 && !no_streamk && tiles % g_sms != 0 && kblocks >= 2;
   StreamK sk{nullptr, nullptr, 0};
   if (use_sk) {
     sk = streamk_for(s);
@@ -1242,7 +1251,7 @@ void debug_gemm(const void* a, const void* w, int M, int N, int K, int epi, cons
                 void* outf, int ldf, int flags, void* stream) {
   const bool force_simt = flags & 1;
   g_force_pair_bn = (flags & 4) ? 128 : (flags & 8) ? 256 : 0;
-  const int streamk_ok = (flags & 16) ? 0 : 1;
+  const int streamk_ok = (flags & 16) ? 0 : (flags & 32) ? 2 : 1;
   if (!(flags & 2)) {
   // The executor keeps weights tile-blocked; the hook takes row-major W.
   static f16* tiled = nullptr;

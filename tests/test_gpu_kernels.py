@@ -121,14 +121,14 @@ def test_decode_gemm_stream_k(M, N, K, epi):
     """Stream-K (whole-tile decode GEMMs over every SM) against the fp32
     reference, the classic tile split (flag 16) and itself (deterministic)."""
     import torch
-    _check(M, N, K, epi)
+    _check(M, N, K, epi, flags=32)
     _check(M, N, K, epi, flags=16)
     torch.manual_seed(1)
     a = (torch.randn(M, K, device="cuda") * 0.5).half()
     w = (torch.randn(N, K, device="cuda") * 0.02).half()
     resid = torch.randn(M, N, device="cuda") if epi == RESID else None
-    x = run_gemm(a, w, epi, None, resid).clone()
-    y = run_gemm(a, w, epi, None, resid).clone()
+    x = run_gemm(a, w, epi, None, resid, flags=32).clone()
+    y = run_gemm(a, w, epi, None, resid, flags=32).clone()
     assert torch.equal(x, y), "stream-K result not deterministic"
 
 
@@ -139,14 +139,14 @@ def test_pair_gemm_stream_k_tail(M, N, K, epi):
     pairs) against the fp32 reference, without the tail (flag 16), and itself
     (deterministic)."""
     import torch
-    _check(M, N, K, epi)
+    _check(M, N, K, epi, flags=32)
     _check(M, N, K, epi, flags=16)
     torch.manual_seed(2)
     a = (torch.randn(M, K, device="cuda") * 0.5).half()
     w = (torch.randn(N, K, device="cuda") * 0.02).half()
     resid = torch.randn(M, N, device="cuda") if epi == RESID else None
-    x = run_gemm(a, w, epi, None, resid).clone()
-    y = run_gemm(a, w, epi, None, resid).clone()
+    x = run_gemm(a, w, epi, None, resid, flags=32).clone()
+    y = run_gemm(a, w, epi, None, resid, flags=32).clone()
     assert torch.equal(x, y), "stream-K tail result not deterministic"
 
 
