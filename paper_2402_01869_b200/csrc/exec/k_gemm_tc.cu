@@ -527,7 +527,8 @@ struct PairSmem {
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 5) * 8 + 16 + 1024;
+  static_assert(STAGES * STAGE_BYTES >= 128 * BN * 4, "a split-tail piece is staged in the drained ring");
 };
 
 __device__ __forceinline__ std::uint32_t cta_rank_in_cluster() {
@@ -648,12 +649,12 @@ __device__ __forceinline__ void epi_cols16(const GemmArgs& a, int m, int n0, flo
 
 // Work of one CTA pair: whole tiles in data-parallel rounds (t = pair,
 // pair + npairs, ...) while every pair has one, then -- split tail (sk.ws
-// set) -- each of the remaining T mod npairs tiles is shared by a group of g
-// = min(4, npairs / rem) pairs, each taking 1/g of its k blocks, instead of
-// one pair per tile while the rest idle through a last partial round.  The
-// group's first pair owns the tile: it waits for the other g - 1 fp32
-// pieces (computed at the same time) and adds them in k order
-// (deterministic).  (Spreading a tail tile over every pair, classic
+// set) -- each of the remaining T mod npairs tiles is shared by a pair of
+// pairs (g = 2 when npairs >= 2 rem), each taking half of its k blocks,
+// instead of one pair per tile while the rest idle through a last partial
+// round.  The group's first pair owns the tile: it bulk-copies the other
+// half's fp32 piece (computed at the same time) into its drained stage ring
+// and adds it after its own (deterministic).  (Spreading a tail tile over every pair, classic
 // stream-K, measured slower: the owner's read of ~17 pieces outweighed the
 // saved k blocks.)
 struct PairSegs {
@@ -669,7 +670,7 @@ struct PairSegs {
     dp_tiles = split_tail ? (tot / np) * np : tot;
     rem = tot - dp_tiles;
     g = rem > 0 ? np / rem : 1;
-    g = g < 1 ? 1 : (g > 4 ? 4 : g);
+    g = g < 1 ? 1 : (g > 2 ? 2 : g);
     g = g > nk ? nk : g;
     dp_next = p;
     tail_done = false;
@@ -691,8 +692,6 @@ struct PairSegs {
     b = (part + 1) * nk / g;
     return true;
   }
-  // pairs holding the later k parts of this pair's tail tile (owner only)
-  __device__ int last_pair_of(int) const { return (pair / g) * g + g - 1; }
 };
 
 template <int BN>
@@ -707,7 +706,8 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
   std::uint64_t* empty = full + STAGES;
   std::uint64_t* tfull = empty + STAGES;  // [2] MMA -> epilogues (multicast)
   std::uint64_t* tempty = tfull + 2;      // [2] epilogues of both CTAs -> MMA (leader's)
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(tempty + 2);
+  std::uint64_t* fixbar = tempty + 2;     // [1] split-tail piece landed in shared memory
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(fixbar + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const std::uint32_t rank = cta_rank_in_cluster();
@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 8);  // 4 epilogue warps x 2 CTAs
     }
+    mbar_init(fixbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   // Both CTAs of the pair must be running before the 2-CTA TMEM allocation:
@@ -850,12 +851,14 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       if (it.a > 0) {
         // A piece of a tail tile owned by an earlier pair: fp32 -> this CTA's slot, publish.
+        // Layout [column chunk][row][16]: the owner reads it back from shared
+        // memory with few bank conflicts.
         float* mine = sk.ws + static_cast<std::int64_t>(blockIdx.x) * (128 * BN);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
           std::uint32_t r[16];
           tmem_ld16(tmem + buf * BN + (static_cast<std::uint32_t>(q * 32) << 16) + c, r);
-          float4* d4 = reinterpret_cast<float4*>(mine + static_cast<std::int64_t>(row) * BN + c);
+          float4* d4 = reinterpret_cast<float4*>(mine + (static_cast<std::int64_t>(c / 16) * 128 + row) * 16);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
             d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
@@ -867,21 +870,38 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
         if (q == 0 && lane == 0)
           asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(sk.flags + blockIdx.x), "r"(sk.epoch) : "memory");
       } else {
-        // Whole tile, or owner of a tail tile: wait for the later pairs' pieces.
-        const int p_last = it.b < nk ? it.last_pair_of(t) : pair;  // a < b < nk only for a split tail owner
-        for (int pp = pair + 1; pp <= p_last; ++pp) {
-          const int cta = 2 * pp + static_cast<int>(rank);
-          const long long t_start = clock64();
-          while (true) {
-            std::int32_t e;
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + cta) : "memory");
-            if (e == sk.epoch) break;
-            if (clock64() - t_start > kWaitLimitCycles) {
-              printf("ib2 watchdog: pair stream-K piece of CTA %d (epoch %d) missing for CTA %d\n", cta, sk.epoch,
-                     blockIdx.x);
-              __trap();
+        // Whole tile, or owner of a split tail tile: wait for the other half's piece,
+        // bulk-copy it into the drained stage ring (the last MMAs have retired:
+        // tfull), add it after this pair's half.
+        const bool owner = it.b < nk;
+        const float* piece_s = reinterpret_cast<const float*>(smem);
+        if (owner) {
+          const int cta = 2 * (pair + 1) + static_cast<int>(rank);
+          if (q == 0 && lane == 0) {
+            const long long t_start = clock64();
+            while (true) {
+              std::int32_t e;
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + cta) : "memory");
+              if (e == sk.epoch) break;
+              if (clock64() - t_start > kWaitLimitCycles) {
+                printf("ib2 watchdog: split-tail piece of CTA %d (epoch %d) missing for CTA %d\n", cta, sk.epoch,
+                       blockIdx.x);
+                __trap();
+              }
             }
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            constexpr std::uint32_t bytes = 128 * BN * 4, part = bytes / 4;
+            mbar_expect_tx(fixbar, bytes);
+            const float* src = sk.ws + static_cast<std::int64_t>(cta) * (128 * BN);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              asm volatile(
+                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                      su32(smem + j * part)),
+                  "l"(reinterpret_cast<std::uint64_t>(src) + j * part), "r"(part), "r"(su32(fixbar))
+                  : "memory");
           }
+          mbar_wait(fixbar, 0);  // used once per kernel: a CTA owns at most one split tail tile
         }
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
@@ -890,13 +910,11 @@ __global__ void __launch_bounds__(256, 1) tc_gemm_pair_kernel(const __grid_const
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-          for (int pp = pair + 1; pp <= p_last; ++pp) {
-            const float4* s4 = reinterpret_cast<const float4*>(
-                sk.ws + static_cast<std::int64_t>(2 * pp + static_cast<int>(rank)) * (128 * BN) +
-                static_cast<std::int64_t>(row) * BN + c);
+          if (owner) {
+            const float4* s4 = reinterpret_cast<const float4*>(piece_s + ((c / 16) * 128 + row) * 16);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 x = __ldcg(s4 + j);
+              const float4 x = s4[j];
               v[4 * j] += x.x;
               v[4 * j + 1] += x.y;
               v[4 * j + 2] += x.z;

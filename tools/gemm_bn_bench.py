@@ -49,11 +49,11 @@ if MODE == "bn":
             print(f"M={M:5d} {name:8s} N={N:6d} K={K:6d}: 256x256 {t256:8.1f} us ({tf / t256 * 1e6:6.0f} TF/s)  "
                   f"256x128 {t128:8.1f} us ({tf / t128 * 1e6:6.0f} TF/s)  best {'128' if t128 < t256 else '256'}")
 else:  # stream-K / split tail on (flags 0) vs off (flag 16), 13B and GPT-J projections
-    for M in (32, 108, 600, 1218, 2048):
+    for M in (32, 108, 600, 1218, 2048) if len(sys.argv) < 3 else [int(x) for x in sys.argv[2].split(",")]:
         for (N, K, epi, name) in ((15360, 5120, STORE, "qkv13"), (5120, 5120, RESID, "o13"), (27648, 5120, SWIGLU, "gu13"),
                                   (5120, 13824, RESID, "down13"), (12288, 4096, STORE, "qkv6"), (16384, 4096, GELU, "fcin6"),
                                   (32000, 5120, STOREF32, "lm13")):
-            ton = time_gemm(M, N, K, epi, 0)
+            ton = time_gemm(M, N, K, epi, 32)
             toff = time_gemm(M, N, K, epi, 16)
             print(f"M={M:5d} {name:7s} N={N:6d} K={K:6d}: split on {ton:8.1f} us  off {toff:8.1f} us  "
                   f"({100 * (toff - ton) / toff:+5.1f} %)")
