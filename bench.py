@@ -393,8 +393,14 @@ def run_b200(args):
                           "peak": link_peak, "peak_h2d": link["h2d"], "peak_d2h": link["d2h"],
                           "frac": swap_gbs / link_peak if swap_gbs else None,
                           "peak_source": "pinned 512 MiB copies measured by bench.py on this box",
-                          "note": "achieved = swapped bytes / time of each PCIe batch on the copy streams; "
-                                  "swap-ins forwarded from swap-out staging do not cross the link"},
+                          "note": "achieved = swapped bytes / time of each PCIe batch on the copy streams "
+                                  "(DMA efficiency while a batch runs); swap-ins forwarded from swap-out staging do "
+                                  "not cross the link; swaps overlap later iterations (cross-iteration pipelining, "
+                                  "not per layer)",
+                          "window_gbs": me["swap_bytes_timed"] / me["dev_s"] / 1e9 if me["dev_s"] else None,
+                          "window_frac": (me["swap_bytes_timed"] / me["dev_s"] / 1e9 / link_peak) if me["dev_s"] else None,
+                          "window_note": "PCIe swap bytes / device time of the timed windows: how much of the link "
+                                         "the workload used under the model step"},
         "roofline": {"bound": "hbm", "kernel": "K1 paged decode attention (middle layer, every timed iteration)",
                      "achieved": k1_gbs, "peak": pk.get("hbm_gbs"), "unit": "GB/s",
                      "frac": (k1_gbs / pk["hbm_gbs"]) if k1_gbs and pk.get("hbm_gbs") else None,
