@@ -1006,10 +1006,13 @@ int g_sms = 0;
 
 StreamK streamk_for(cudaStream_t s);
 
-// GemmArgs::streamk_ok: 0 never, 1 if enabled (IB2_STREAMK=1), 2 forced (tests).
-bool streamk_enabled(const GemmArgs& a) {
-  static const bool env_on = getenv("IB2_STREAMK") != nullptr;
-  return a.streamk_ok == 2 || (a.streamk_ok == 1 && env_on);
+// GemmArgs::streamk_ok: 0 never, 1 if enabled, 2 forced (tests).  The pair
+// GEMM's split tail is on by default (C4: 42.3 -> 41.9 ms per iteration, A/B
+// in profiles/r2q; IB2_NO_SPLIT_TAIL=1 turns it off); the decode GEMM's
+// stream-K is opt-in (IB2_STREAMK=1; measured slower, profiles/r2o).
+bool streamk_enabled(const GemmArgs& a, bool pair_tail = false) {
+  static const bool sk_on = getenv("IB2_STREAMK") != nullptr, tail_on = getenv("IB2_NO_SPLIT_TAIL") == nullptr;
+  return a.streamk_ok == 2 || (a.streamk_ok == 1 && (pair_tail ? tail_on : sk_on));
 }
 
 template <int BN>
@@ -1027,7 +1030,7 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   // Tiles that do not divide into whole rounds over the pairs: split tail
   // (PairSegs; compute stream only, see StreamK).
   static const bool no_streamk = getenv("IB2_NO_STREAMK") != nullptr;  // diagnostics
-  const bool use_sk = streamk_enabled(a) && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
+  const bool use_sk = streamk_enabled(a, true) && !no_streamk && tiles % (g_sms / 2) != 0 && a.K / BK >= 2;
   const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
   const int pairs = use_sk ? g_sms / 2 : std::max(1, std::min(g_sms / 2, tiles));
   cudaLaunchConfig_t cfg{};

@@ -148,69 +148,6 @@ __global__ void __launch_bounds__(NT) norm_kernel(const float* __restrict__ x, i
   }
 }
 
-// Vector variant for D % 8 == 0: one 128-thread CTA per row, NV float4 per
-// thread (16-byte loads, 8-byte f16 stores), two block reductions over 4 warps.
-template <int NV>
-__global__ void __launch_bounds__(128) norm_vec_kernel(const float* __restrict__ x, int ldx,
-                                                      const std::int32_t* __restrict__ row_index, int D,
-                                                      const f16* __restrict__ gamma, const f16* __restrict__ beta,
-                                                      int rms, float eps, f16* __restrict__ y, int ldy) {
-  pdl_trigger();
-  pdl_wait();
-  __shared__ float red[4];
-  const int r = blockIdx.x;
-  const int src = row_index ? row_index[r] : r;
-  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<std::int64_t>(src) * ldx);
-  const int nv = D / 4;
-  float4 v[NV];
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = threadIdx.x + i * 128;
-    v[i] = c < nv ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
-  float mean = 0.f;
-  if (!rms) mean = block_sum<128>(s, red) / D;
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = threadIdx.x + i * 128;
-    if (c < nv) {
-      const float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, d = v[i].w - mean;
-      q += (a * a + b * b) + (cc * cc + d * d);
-    }
-  }
-  const float var = block_sum<128>(q, red) / D;
-  const float inv = rsqrtf(var + eps);
-  f16* yr = y + static_cast<std::int64_t>(r) * ldy;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = threadIdx.x + i * 128;
-    if (c < nv) {
-      const uint2 gu = reinterpret_cast<const uint2*>(gamma)[c];
-      const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gu.x));
-      const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gu.y));
-      float o0 = (v[i].x - mean) * inv * g01.x, o1 = (v[i].y - mean) * inv * g01.y;
-      float o2 = (v[i].z - mean) * inv * g23.x, o3 = (v[i].w - mean) * inv * g23.y;
-      if (beta) {
-        const uint2 bu = reinterpret_cast<const uint2*>(beta)[c];
-        const float2 b01 = __half22float2(*reinterpret_cast<const __half2*>(&bu.x));
-        const float2 b23 = __half22float2(*reinterpret_cast<const __half2*>(&bu.y));
-        o0 += b01.x;
-        o1 += b01.y;
-        o2 += b23.x;
-        o3 += b23.y;
-      }
-      const __half2 h01 = __floats2half2_rn(o0, o1), h23 = __floats2half2_rn(o2, o3);
-      uint2 out;
-      out.x = *reinterpret_cast<const std::uint32_t*>(&h01);
-      out.y = *reinterpret_cast<const std::uint32_t*>(&h23);
-      reinterpret_cast<uint2*>(yr)[c] = out;
-    }
-  }
-}
-
 // Per row: rotate q and k of every head (fp32, no contraction, matching the
 // oracle's float32 arithmetic), round to f16, and store k, v into the row's
 // paged slot.
@@ -466,17 +403,6 @@ void launch_embed(const RowDesc* rows, int n, std::int32_t* hist, int hist_strid
 void launch_norm(const float* x, int ldx, const std::int32_t* row_index, int n, int D, const f16* gamma,
                  const f16* beta, bool rms, float eps, f16* y, int ldy, cudaStream_t s) {
   if (n <= 0) return;
-  const bool vec = D % 8 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && D <= 8192 && getenv("IB2_SCALAR_NORM") == nullptr;
-  if (vec) {
-    const int nv = (D / 4 + 127) / 128;
-    if (nv <= 1) launch_pdl(norm_vec_kernel<1>, dim3(n), dim3(128), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
-    else if (nv <= 2) launch_pdl(norm_vec_kernel<2>, dim3(n), dim3(128), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
-    else if (nv <= 4) launch_pdl(norm_vec_kernel<4>, dim3(n), dim3(128), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
-    else if (nv <= 8) launch_pdl(norm_vec_kernel<8>, dim3(n), dim3(128), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
-    else launch_pdl(norm_vec_kernel<16>, dim3(n), dim3(128), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
-    IB2_LAUNCH_CHECK();
-    return;
-  }
   if (D <= 1024) {
     launch_pdl(norm_kernel<256, 4>, dim3(n), dim3(256), 0, s, x, ldx, row_index, D, gamma, beta, static_cast<int>(rms), eps, y, ldy);
   } else if (D <= 4096) {
