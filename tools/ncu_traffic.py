@@ -16,5 +16,6 @@ json.dump({"kernel": r[hdr.index("Kernel Name")].split("(")[0], "dram_bytes_per_
            "algorithmic_bytes_per_launch": h["k1_algorithmic_bytes_first_decode_layer"],
            "ratio": traffic / h["k1_algorithmic_bytes_first_decode_layer"],
            "source": f"ncu --set full of {rep.split('/')[-1]} on tools/prof_harness.py "
-                     f"({h['requests']} decode rows, context {h['ctx']}, GPT-J shape)"}, open(out, "w"), indent=1)
+                     f"({h['requests']} decode rows, context {h['ctx']}, {h.get('preset', 'gptj-6b')} shape, "
+                     f"{h.get('layers', 28)} layers)"}, open(out, "w"), indent=1)
 print(open(out).read())

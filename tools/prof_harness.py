@@ -6,7 +6,7 @@ plans that reproduce the C1 window's kernel shapes with a small KV pool, so
            (chunk rows -> K2 + CTA-pair GEMMs), chunked like the scheduler;
   phase 2  D decode iterations over all R requests (K1 + split-K GEMMs).
 
-Usage: python tools/prof_harness.py [R=30] [CTX=1100] [D=6]
+Usage: python tools/prof_harness.py [R=30] [CTX=1100] [D=6] [preset=gptj-6b] [layers]
 Prints the algorithmic K1 bytes of one decode layer (for the ncu traffic
 comparison) and the device time of the decode iterations.
 """
@@ -21,12 +21,14 @@ GROW, DECODE, FRESH = 0, 0, 1
 R = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 CTX = int(sys.argv[2]) if len(sys.argv) > 2 else 1100
 ND = int(sys.argv[3]) if len(sys.argv) > 3 else 6
+PRESET = sys.argv[4] if len(sys.argv) > 4 else "gptj-6b"
+LAYERS = int(sys.argv[5]) if len(sys.argv) > 5 else {"gptj-6b": 28, "vicuna-13b": 40}[PRESET]
 PER = max(1, 3300 // CTX)
-D_MODEL, LAYERS = 4096, 28
+D_MODEL = {"gptj-6b": 4096, "vicuna-13b": 5120}[PRESET]
 
 blocks = R * ((CTX + ND + 16) // 16 + 1) + 64
-ex = ib.Executor({"preset": "gptj-6b"}, 0, dict(gpu_blocks=blocks, host_bytes=64 << 20, max_requests=max(64, R),
-                                                  max_rows=4096, timing=True))
+ex = ib.Executor({"preset": PRESET, "layers": LAYERS}, 0,
+                 dict(gpu_blocks=blocks, host_bytes=64 << 20, max_requests=max(64, R), max_rows=4096, timing=True))
 it = 0
 
 
@@ -54,6 +56,7 @@ ex.mark(1)
 ex.sync()
 ms = ex.elapsed_ms()
 st = ex.stats()
-print(json.dumps({"requests": R, "ctx": CTX, "decode_iterations": ND, "decode_ms_per_iteration": ms / ND,
+print(json.dumps({"preset": PRESET, "layers": LAYERS, "requests": R, "ctx": CTX, "decode_iterations": ND,
+                  "decode_ms_per_iteration": ms / ND,
                   "k1_algorithmic_bytes_first_decode_layer": k1_bytes,
                   "k1_gbs_timed_layer": st["k1_bytes"] / (st["k1_ms"] / 1e3) / 1e9 if st["k1_ms"] else None}))
