@@ -80,7 +80,9 @@ struct SkSmem {
   static constexpr int PART_BYTES = NT * BM * 4;  // one fp32 partial tile
   static constexpr int PART_OFF = STAGES * STAGE_BYTES;
   static constexpr int BAR_OFF = PART_OFF + PART_SLOTS * PART_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 8) * 8 + 16 + 1024;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 9) * 8 + 16 + 1024;
+  // stream-K: an owner stages up to two fp32 pieces in its drained ring
+  static_assert(NT > 128 || STAGES * STAGE_BYTES >= 2 * NT * BM * 4, "stream-K pieces fit in the ring");
   static constexpr int TMEM_COLS = 2 * NT < 32 ? 32 : 2 * NT;
   static_assert(TOTAL <= 232448, "shared memory budget");
 };
@@ -239,7 +241,8 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   std::uint64_t* tempty = tfull + 2;      // [2] epilogue -> MMA
   std::uint64_t* ready = tempty + 2;      // [2] all ranks' partials of a slot written
   std::uint64_t* consumed = ready + 2;    // [2] all ranks done reading a slot
-  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(consumed + 2);
+  std::uint64_t* fixbar = consumed + 2;   // [1] stream-K pieces landed in the ring
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(fixbar + 1);
   float* parts = reinterpret_cast<float*>(smem + L::PART_OFF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
       mbar_init(&ready[i], 4 * S);
       mbar_init(&consumed[i], 4 * S);
     }
+    mbar_init(fixbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -400,22 +404,43 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
           if (q == 0 && lane == 0)
             asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(sk.flags + blockIdx.x), "r"(sk.epoch) : "memory");
         } else {
-          // Whole tile, or the owner of a tile whose later k blocks are pieces of the next CTAs.
+          // Whole tile, or the owner of a tile whose later k blocks are pieces of
+          // the next CTAs (at most two): their fp32 slots are bulk-copied into
+          // this CTA's drained stage ring (its last MMAs retired: tfull), then
+          // added after this CTA's own partial, in k order.
           const int c_last = kbe < kblocks ? sk_cta_of(static_cast<long long>(t + 1) * kblocks - 1, total_u, gridDim.x)
                                            : static_cast<int>(blockIdx.x);
-          for (int p = blockIdx.x + 1; p <= c_last; ++p) {
-            const long long t_start = clock64();
-            while (true) {
-              std::int32_t e;
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + p) : "memory");
-              if (e == sk.epoch) break;
-              if (clock64() - t_start > kWaitLimitCycles) {
-                printf("ib2 watchdog: stream-K piece of CTA %d (epoch %d) missing for CTA %d\n", p, sk.epoch,
-                       blockIdx.x);
-                __trap();
+          const int npieces = c_last - static_cast<int>(blockIdx.x);
+          if (npieces > 2) __trap();  // the grid planner keeps >= kblocks / 2 units per CTA
+          if (npieces > 0) {
+            if (q == 0 && lane == 0) {
+              for (int p = blockIdx.x + 1; p <= c_last; ++p) {
+                const long long t_start = clock64();
+                while (true) {
+                  std::int32_t e;
+                  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(e) : "l"(sk.flags + p) : "memory");
+                  if (e == sk.epoch) break;
+                  if (clock64() - t_start > kWaitLimitCycles) {
+                    printf("ib2 watchdog: stream-K piece of CTA %d (epoch %d) missing for CTA %d\n", p, sk.epoch,
+                           blockIdx.x);
+                    __trap();
+                  }
+                }
               }
+              asm volatile("fence.proxy.async.global;\n" ::: "memory");
+              constexpr std::uint32_t bytes = NT * BM * 4;
+              mbar_expect_tx(fixbar, bytes * npieces);
+              for (int k = 0; k < npieces; ++k)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                        su32(smem + k * bytes)),
+                    "l"(reinterpret_cast<std::uint64_t>(sk.ws + static_cast<std::int64_t>(blockIdx.x + 1 + k) * (NT * BM))),
+                    "r"(bytes), "r"(su32(fixbar))
+                    : "memory");
             }
+            mbar_wait(fixbar, 0);  // once per kernel: a CTA owns at most one partial tile
           }
+          const float* staged = reinterpret_cast<const float*>(smem);
 #pragma unroll 1
           for (int cc = 0; cc < mcols; cc += 16) {
             std::uint32_t r[16];
@@ -423,10 +448,10 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
             float v[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-            for (int p = blockIdx.x + 1; p <= c_last; ++p) {
-              const float* piece = sk.ws + static_cast<std::int64_t>(p) * (NT * BM);
+            for (int k = 0; k < npieces; ++k) {
+              const float* piece = staged + static_cast<std::int64_t>(k) * (NT * BM);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] += __ldcg(piece + (cc + j) * BM + row);
+              for (int j = 0; j < 16; ++j) v[j] += piece[(cc + j) * BM + row];
             }
             epi_rows16(args, n, cc, v, lane);
           }
@@ -1165,11 +1190,13 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   // per GEMM (profiles/r2o/streamk_per_gemm.txt) it wins on a few shapes
   // (GPT-J QKV at M = 32: +9 %) and loses on more (M = 108: -14..-26 %), and
   // C4 end to end ran 2.3 % slower with it.
-  const bool use_sk = streamk_enabled(a) && sp.S == 1 && !no_streamk && tiles % g_sms != 0 && kblocks >= 2;
+  const bool use_sk = NT <= 128 && streamk_enabled(a) && sp.S == 1 && !no_streamk && tiles % g_sms != 0 &&
+                      kblocks >= 2;
   StreamK sk{nullptr, nullptr, 0};
   if (use_sk) {
     sk = streamk_for(s);
-    sp.clusters = std::min<long long>(g_sms, static_cast<long long>(tiles) * kblocks);
+    // at least kblocks / 2 units per CTA: a tile spans at most 3 CTAs (<= 2 pieces)
+    sp.clusters = static_cast<int>(std::min<long long>(g_sms, (2LL * tiles * kblocks) / std::max(1, kblocks)));
   }
   if (verbose)
     fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d%s\n", a.N, a.K, a.M, sp.S, sp.clusters,
