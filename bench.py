@@ -299,6 +299,7 @@ def run_b200(args):
     acc = {k: 0.0 for k in keys}
     acc.update(dev_s=0.0, wall_s=0.0, completed=0, decode=0, swapped=0)
     pos = 0
+    win_ms = []  # device ms per iteration of each window
     profiling = os.environ.get("BENCH_PROFILE") == "1"
     for (start, count) in wins:
         if start - args.warmup > pos:
@@ -328,6 +329,7 @@ def run_b200(args):
             raise SystemExit(f"schedule ended inside a timed window ({done} of {count})")
         pos += done
         c1, s1 = sess.counters(), ex.stats()
+        win_ms.append(round(ex.elapsed_ms() / count, 3))
         acc["dev_s"] += ex.elapsed_ms() / 1e3
         acc["wall_s"] += wall
         acc["completed"] += c1["completed"] - c0["completed"]
@@ -337,7 +339,7 @@ def run_b200(args):
             acc[k] += s1[k] - s0[k]
     clk = clocks.stop()
     host_peak = ex.stats()["host_pool_peak"]
-    local_stats = dict(acc, iters=total_iters, total_done=total_done, host_peak=host_peak)
+    local_stats = dict(acc, iters=total_iters, total_done=total_done, host_peak=host_peak, win_ms=win_ms)
     if dist:
         gathered = [None] * world
         dist.all_gather_object(gathered, local_stats)
@@ -375,6 +377,7 @@ def run_b200(args):
                                 "bit-exact schedule x measured device seconds per iteration); the timed iterations "
                                 "are a stratified sample of each schedule",
                    "windows": [[s, c] for s, c in wins], "warmup_per_window": args.warmup,
+                   "window_ms_per_iteration": [g["win_ms"] for g in gathered],
                    "schedule_iterations": [g["iters"] for g in gathered],
                    "l2": cfg["l2"]},
         "decode_tok_s": tot["decode"] / dev_s_max,
