@@ -6,6 +6,7 @@ stall, fire/done/evict/swapin events, and per-request ledger snapshots) must be
 byte-identical (ledger key order aside), and so must the summaries and the
 per-request CSVs.  Reference: proj/src/engine.cpp:282-581.
 """
+import json
 import os
 
 import pytest
@@ -79,3 +80,29 @@ def test_fractional_memory_and_fit(tmp_path):
     # Non-integral mem_per_token exercises the double byte totals (memory.cpp:17).
     cost = dict(C0_COST, mem_per_token=3000.7, gpu_kv_capacity=16384 * 3000.7 * 1.01)
     check(dict(C0_WORKLOAD, request_count=32), cost, dict(policy="infercept", dump_ledger_every=1), tmp_path)
+
+
+@pytest.mark.parametrize("workload", [
+    "C0", dict(classes=[{"name": "Math"}, {"name": "QA"}, {"name": "Chatbot"}], request_count=300, arrival_rate=3.0, seed=11),
+    dict(classes=[{"name": c} for c in ["Math", "QA", "VE", "Chatbot", "Image", "TTS"]], request_count=500,
+         arrival_rate=1000.0, seed=23),
+])
+def test_saved_trace_jsonl_byte_identical(tmp_path, workload):
+    """f3: a trace generated and saved by the product library is byte-identical
+    to the reference's (proj/src/workload.cpp generation, trace_io.cpp format)."""
+    import ctypes
+    from conftest import C0_WORKLOAD, PRODUCT_LIB, REF_LIB
+    wl = C0_WORKLOAD if workload == "C0" else workload
+    outs = []
+    for lib_path, tag in ((REF_LIB, "ref"), (PRODUCT_LIB, "ours")):
+        L = ctypes.CDLL(lib_path)
+        L.isim_trace_generate.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.isim_trace_save.argtypes = [ctypes.c_void_p, ctypes.c_char_p]
+        L.isim_trace_free.argtypes = [ctypes.c_void_p]
+        t = ctypes.c_void_p()
+        assert L.isim_trace_generate(json.dumps(wl).encode(), ctypes.byref(t)) == 0
+        path = str(tmp_path / f"{tag}.jsonl")
+        assert L.isim_trace_save(t, path.encode()) == 0
+        L.isim_trace_free(t)
+        outs.append(open(path, "rb").read())
+    assert outs[0] == outs[1] and len(outs[0]) > 1000
