@@ -545,6 +545,11 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
+    from oracle.ref_plans import REF_LIB
+    if not os.path.exists(REF_LIB):
+        print(json.dumps({"impl": "reference", "unavailable": f"{REF_LIB} not built (make -C oracle needs "
+                                                              f"/root/reference)"}))
+        return
     # Same window positions as the B200 arm at N = 1 (the whole trace, one host).
     from oracle.ref_plans import run_reference as ref_run
     summ = ref_run(cfg["workload"], cfg["cost"], RUN, None)
