@@ -417,7 +417,11 @@ def run_b200(args):
         "gpu_launches": int(tot["kernel_launches"]),
         "clocks": clk,
     }
-    if world == 1 and not args.no_cpu_baseline:
+    from oracle.ref_plans import REF_LIB
+    if world == 1 and not args.no_cpu_baseline and not os.path.exists(REF_LIB):
+        line["cpu_baseline"] = {"value": None, "unit": "req/s", "cores": os.cpu_count(), "kind": "reference",
+                                "sample": f"unavailable: {REF_LIB} not built"}
+    elif world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(cfg, args, wins)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "req/s", "cores": cpu["cores"], "kind": "port",
                                 "sample": cpu["sample"], "s_per_iteration": cpu["s_per_iteration"]}
