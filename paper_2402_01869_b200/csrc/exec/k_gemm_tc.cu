@@ -1232,6 +1232,8 @@ void launch_skinny_any(const GemmArgs& a, cudaStream_t s) {
     IB2_CUDA(cudaGetDevice(&dev));
     IB2_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  // (Deeper weight rings -- 11 / 9 stages for M <= 16 / 32 -- measured
+  // identical per GEMM: the ring is not what limits the weight stream.)
   if (a.M <= 16) launch_skinny<16, 10>(a, s);
   else if (a.M <= 32) launch_skinny<32, 8>(a, s);
   else if (a.M <= 64) launch_skinny<64, 6>(a, s);

@@ -39,6 +39,14 @@ def time_gemm(M, N, K, epi, flags, reps=20):
 
 
 MODE = sys.argv[1] if len(sys.argv) > 1 else "bn"
+if MODE == "plain":  # one timing per shape at the current settings (env-driven A/B)
+    for M in [int(x) for x in sys.argv[2].split(",")]:
+        for (N, K, epi, name) in ((15360, 5120, STORE, "qkv13"), (27648, 5120, SWIGLU, "gu13"), (12288, 4096, STORE, "qkv6"),
+                                  (16384, 4096, GELU, "fcin6"), (4096, 4096, RESID, "o6"), (4096, 16384, RESID, "fcout6"),
+                                  (50400, 4096, STOREF32, "lm6")):
+            t = time_gemm(M, N, K, epi, 0)
+            print(f"M={M:4d} {name:7s} {t:8.1f} us  {N * K * 2 / t / 1e3:7.0f} GB/s")
+    sys.exit(0)
 if MODE == "bn":
     for M in (600, 1218, 2048):
         for (N, K, epi, name) in ((15360, 5120, STORE, "qkv"), (5120, 5120, RESID, "o"), (27648, 5120, SWIGLU, "gate_up"),
