@@ -165,3 +165,13 @@ def test_end_to_end_run_with_executor_matches_scheduler_only_run():
     b = ib.run(t, m, dict(policy="infercept", executor="b200",
                           exec={"model": {"preset": "tiny"}, "pools": pools_for(C0_COST, 2048, record=False)})).summary()
     assert a == b
+
+
+@pytest.mark.skipif(not have_gpu(), reason="needs a B200")
+def test_split_batch_option_parity(c0_plans):
+    # The opt-in split_batch executor (decode rows and chunk rows as two
+    # micro-batches on two streams; measured slower, kept for experiments)
+    # against the oracle on the first 1,500 C0 iterations.
+    plans, _ = c0_plans
+    r = replay(plans, {"preset": "tiny"}, pools_for(C0_COST, 2048, split_batch=True), 1500, check_tables_every=10)
+    assert r["sampled"] > 1000 and r["kv_checked"] > 0
