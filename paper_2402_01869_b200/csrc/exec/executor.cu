@@ -241,7 +241,6 @@ class Impl final : public B200Executor {
   float* rope_cs_ = nullptr;
   float *x_ = nullptr, *logits_ = nullptr, *part_o_ = nullptr, *part_ml_ = nullptr;
   std::int32_t* k1_counters_ = nullptr;  // K1 split arrival counters (last split merges)
-  std::int32_t* k1_queue_ = nullptr;     // K1 work queues [2 streams][2] (persistent grid)
   f16 *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *hid_ = nullptr, *lmrows_ = nullptr;
   std::int32_t* out_tok_ = nullptr;
 
@@ -489,8 +488,6 @@ Impl::Impl(const std::string& model_json, int device, const std::string& pools_j
   part_ml_ = dalloc<float>(max_samples * spec_.heads * max_splits * 2);
   k1_counters_ = dalloc<std::int32_t>(max_samples * spec_.heads);
   IB2_CUDA(cudaMemsetAsync(k1_counters_, 0, max_samples * spec_.heads * 4, main_));
-  k1_queue_ = dalloc<std::int32_t>(4);
-  IB2_CUDA(cudaMemsetAsync(k1_queue_, 0, 4 * 4, main_));
   set_gemm_activation_rows(max_rows_);
   chunk_ws_o_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * spec_.head_dim());
   chunk_ws_ml_ = dalloc<float>(static_cast<std::size_t>(kMaxChunkParts) * kChunkTileRows * 2);
@@ -582,7 +579,7 @@ Impl::~Impl() {
     cudaEventDestroy(b->consumed);
   }
   void* ptrs[] = {weights_, pool_, table_, stack_, top_, err_, hist_, rope_cs_, x_, xn_, qkv_, attn_, hid_, lmrows_,
-                  logits_, out_tok_, part_o_, part_ml_, k1_counters_, k1_queue_, chunk_ws_o_, chunk_ws_ml_};
+                  logits_, out_tok_, part_o_, part_ml_, k1_counters_, chunk_ws_o_, chunk_ws_ml_};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   cudaStreamDestroy(main_);
@@ -1285,7 +1282,7 @@ void Impl::forward(int n, int n_drows, int n_tiles, int n_samples) {
         IB2_CUDA(cudaEventRecord(e0, st));
       }
       launch_decode_attention(qkv_, drows_dev_, rows_dev_, n_drows, g, l, max_pos1_, part_o_, part_ml_, attn_,
-                              k1_counters_, k1_queue_ + (st == main_ ? 0 : 2), st);
+                              k1_counters_, st);
       if (n_drows) ++kernel_launches_;
       if (time_k1) {
         IB2_CUDA(cudaEventRecord(e1, st));

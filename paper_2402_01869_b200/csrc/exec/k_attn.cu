@@ -9,9 +9,7 @@
 // algorithmic bytes = 2 * ctx * hd * 2 per (row, head).
 //
 // K2 (chunk rows) lives in k_attn_chunk.cu (tcgen05 + TMEM + TMA).
-#include <algorithm>
 #include <cfloat>
-#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -36,22 +34,23 @@ __device__ __forceinline__ void h8_to_f32(const uint4& u, float* f) {
 // Occupancy: at head_dim 256 the unconstrained kernel takes 96 registers (5
 // CTAs per SM); capping it at 80 (6 CTAs per SM, 28 B of spills) measured
 // +2 % K1 bandwidth on the C1 window, a cap of 7 CTAs -4 % (profiles/r1j).
-// Work items (split, head, decode row) are handed out by a queue: a grid of
-// SMs x resident CTAs loops `item = atomicAdd(queue)` until the items run out
-// (persistent), so the last wave is not a partial one; the last CTA to leave
-// re-arms the queue for the next launch.  (queue = nullptr: one CTA per item,
-// grid (max_splits, H, rows).)
 template <int HD>
 __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn_kernel(
     const f16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
     const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
     const std::int32_t* __restrict__ table, int max_lb, int H, int max_splits, float* __restrict__ part_o,
-    float* __restrict__ part_ml, f16* __restrict__ out, std::int32_t* __restrict__ counters,
-    std::int32_t* __restrict__ queue, int n_items) {
+    float* __restrict__ part_ml, f16* __restrict__ out, std::int32_t* __restrict__ counters) {
   pdl_trigger();
   pdl_wait();
   constexpr int LPT = HD / 8;   // lanes per token
   constexpr int TPW = 32 / LPT; // tokens per warp step
+  const int split = blockIdx.x, h = blockIdx.y, dr = blockIdx.z;
+  const int r = drow[dr];
+  const RowDesc d = rows[r];
+  const int ctx = d.pos + 1;
+  const int start = split * kSplit;
+  if (start >= ctx) return;
+  const int end = min(ctx, start + kSplit);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPT, grp = lane / LPT;
   const int D = H * HD;
@@ -59,31 +58,6 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
   __shared__ float s_score[kSplit];
   __shared__ float s_red[kDecWarps];
   __shared__ float s_acc[kDecWarps][HD];
-  __shared__ int s_item;
-  __shared__ int s_last;
-  for (int round = 0;; ++round) {
-  int split, h, dr;
-  if (queue) {
-    if (threadIdx.x == 0) s_item = atomicAdd(&queue[0], 1);
-    __syncthreads();
-    const int item = s_item;
-    __syncthreads();
-    if (item >= n_items) break;
-    split = item % max_splits;
-    h = (item / max_splits) % H;
-    dr = item / (max_splits * H);
-  } else {
-    if (round > 0) break;
-    split = blockIdx.x;
-    h = blockIdx.y;
-    dr = blockIdx.z;
-  }
-  const int r = drow[dr];
-  const RowDesc d = rows[r];
-  const int ctx = d.pos + 1;
-  const int start = split * kSplit;
-  if (start >= ctx) continue;
-  const int end = min(ctx, start + kSplit);
 
   float q[8];
   {
@@ -186,6 +160,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
   // The last split of this (row, head) to finish merges all splits (in split
   // order, so the result does not depend on which CTA is last) and re-arms
   // the counter: no separate combine launch, and the merge runs in K1's tail.
+  __shared__ int s_last;
   const int ns = (ctx + kSplit - 1) / kSplit;
   __threadfence();
   __syncthreads();
@@ -195,7 +170,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
     if (s_last) counters[dr * H + h] = 0;
   }
   __syncthreads();
-  if (!s_last) continue;
+  if (!s_last) return;
   __threadfence();
   const std::int64_t pb = (static_cast<std::int64_t>(dr) * H + h) * max_splits;
   float M = -FLT_MAX;
@@ -208,42 +183,17 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
     for (int sp = 0; sp < ns; ++sp) o += __ldcg(&part_o[(pb + sp) * HD + i]) * exp2f(__ldcg(&part_ml[(pb + sp) * 2]) - M);
     out[static_cast<std::int64_t>(r) * D + h * HD + i] = __float2half_rn(o * inv);
   }
-  __syncthreads();  // shared buffers are reused by the next item
-  }
-  if (queue && threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&queue[1], 1) == static_cast<int>(gridDim.x) - 1) {
-      queue[0] = 0;
-      queue[1] = 0;
-    }
-  }
 }
 
 template <int HD>
 void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
                       int layer, int max_pos1, float* part_o, float* part_ml, f16* out,
-                      std::int32_t* counters, std::int32_t* queue, cudaStream_t s) {
+                      std::int32_t* counters, cudaStream_t s) {
   const int max_splits = (max_pos1 + kSplit - 1) / kSplit;
-  const long long items = static_cast<long long>(max_splits) * g.heads * n;
-  static const bool fixed_grid = getenv("IB2_K1_GRID") != nullptr;  // diagnostics: one CTA per item
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 0, per = 0;
-    IB2_CUDA(cudaGetDevice(&dev));
-    IB2_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    IB2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, decode_attn_kernel<HD>, kDecWarps * 32, 0));
-    slots = sms * std::max(per, 1);
-  }
-  if (fixed_grid || !queue || items <= slots || items > (1LL << 30)) {
-    dim3 grid(max_splits, g.heads, n);
-    launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
-               layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o,
-               part_ml, out, counters, static_cast<std::int32_t*>(nullptr), 0);
-  } else {
-    launch_pdl(decode_attn_kernel<HD>, dim3(slots), dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
-               layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o,
-               part_ml, out, counters, queue, static_cast<int>(items));
-  }
+  dim3 grid(max_splits, g.heads, n);
+  launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
+             layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml,
+             out, counters);
   IB2_LAUNCH_CHECK();
 }
 
@@ -251,12 +201,12 @@ void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* r
 
 void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
-                             f16* out, std::int32_t* counters, std::int32_t* queue, cudaStream_t s) {
+                             f16* out, std::int32_t* counters, cudaStream_t s) {
   if (n_drows <= 0) return;
   switch (g.head_dim) {
-    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, queue, s); break;
-    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, queue, s); break;
-    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, queue, s); break;
+    case 64: launch_decode_hd<64>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
+    case 128: launch_decode_hd<128>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
+    case 256: launch_decode_hd<256>(qkv, drow, rows, n_drows, g, layer, max_pos_plus1, part_o, part_ml, out, counters, s); break;
     default: throw DeviceError("unsupported head_dim");
   }
 }

@@ -42,8 +42,7 @@ void launch_rope_kv_write(f16* qkv, const RowDesc* rows, int n, const KvGeom& g,
 // K1: split-KV paged decode attention for single rows.
 void launch_decode_attention(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n_drows,
                              const KvGeom& g, int layer, int max_pos_plus1, float* part_o, float* part_ml,
-                             f16* out, std::int32_t* counters, std::int32_t* queue, cudaStream_t s);
-// queue: 2 int32, zero before the first launch (work-queue K1; K1 re-arms it); per stream.
+                             f16* out, std::int32_t* counters, cudaStream_t s);
 // counters: n_rows x heads int32, zero before the first launch; K1 leaves them zero.
 
 // K2: tiled causal attention over the paged prefix for chunk rows, split-KV
