@@ -231,7 +231,7 @@ __device__ __forceinline__ int sk_cta_of(long long u, long long total, int G) {
 template <int NT, int STAGES>
 __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant__ CUtensorMap map_w,
                                                            const __grid_constant__ CUtensorMap map_a, GemmArgs args,
-                                                           int S, StreamK sk, int mc) {
+                                                           int S, StreamK sk) {
   using L = SkSmem<NT, STAGES>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -249,11 +249,8 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   const int tiles = (args.N + BM - 1) / BM, kblocks = args.K / BK;
   const int rank = S > 1 ? static_cast<int>(cluster_rank()) : 0;
   const int n_clusters = gridDim.x / S, cid = blockIdx.x / S;
-  // mc: whole tiles, one per CTA, CTAs paired in a cluster that shares the
-  // activation tile: each loads half of its rows and multicasts it to both.
-  const std::uint32_t crank = mc ? cluster_rank() : 0;
-  const int t0 = mc ? static_cast<int>(blockIdx.x) : static_cast<int>(static_cast<long long>(cid) * tiles / n_clusters);
-  const int t1 = mc ? t0 + 1 : static_cast<int>(static_cast<long long>(cid + 1) * tiles / n_clusters);
+  const int t0 = static_cast<int>(static_cast<long long>(cid) * tiles / n_clusters);
+  const int t1 = static_cast<int>(static_cast<long long>(cid + 1) * tiles / n_clusters);
   const int kb0 = rank * kblocks / S, kb1 = (rank + 1) * kblocks / S;
   // Segments of this CTA: (tile, [kb_a, kb_b)).  Cluster split-K / whole
   // tiles: t0..t1 with [kb0, kb1).  Stream-K: the unit range [u0, u1).
@@ -279,7 +276,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
     asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<std::uint64_t>(&map_a)) : "memory");
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], mc ? 2 : 1);  // mc: both CTAs' MMAs must be done with the shared activation rows
+      mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -297,25 +294,11 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (S > 1 || mc) {  // peers' barriers are initialised before anyone signals them
+  if (S > 1) {  // peers' barriers are initialised before anyone signals them
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const std::uint32_t tmem = *tmem_slot;
-  // Activation tile of k block kb into stage st: whole (local) or this CTA's
-  // half multicast to both CTAs of the cluster (same shared-memory offset).
-  auto load_a = [&](unsigned char* dst, std::uint64_t* bar, int kb) {
-    if (!mc) {
-      tma_load_2d(dst, &map_a, bar, kb * BK, 0);
-      return;
-    }
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
-        "[%0], [%1, {%3, %4}], [%2], %5;\n" ::"r"(su32(dst + crank * (NT / 2) * 128)),
-        "l"(reinterpret_cast<std::uint64_t>(&map_a)), "r"(su32(bar)), "r"(kb * BK), "r"(static_cast<int>(crank) * (NT / 2)),
-        "h"(static_cast<unsigned short>(3))
-        : "memory");
-  };
   pdl_trigger();
 
   if (warp == 0) {
@@ -337,7 +320,8 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
         }
       }
       pdl_wait();
-      for (int i = 0; i < early; ++i) load_a(smem + i * L::STAGE_BYTES + L::A_BYTES, &full[i], early_kb[i]);
+      for (int i = 0; i < early; ++i)
+        tma_load_2d(smem + i * L::STAGE_BYTES + L::A_BYTES, &map_a, &full[i], early_kb[i] * BK, 0);
       int i = 0;
       for (int t = seg_first_t; t < seg_end_t; ++t) {
         int a, b;
@@ -349,7 +333,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
           unsigned char* sw = smem + st * L::STAGE_BYTES;
           mbar_expect_tx(&full[st], L::STAGE_BYTES);
           tma_load_2d(sw, &map_w, &full[st], 0, (t * kblocks + kb) * BM);  // one contiguous 16 KB tile
-          load_a(sw + L::A_BYTES, &full[st], kb);
+          tma_load_2d(sw + L::A_BYTES, &map_a, &full[st], kb * BK, 0);
         }
       }
     }
@@ -382,16 +366,9 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
                 "}\n" ::"r"(acc_tmem),
                 "l"(da + 2 * k), "l"(db + 2 * k), "r"(idesc), "r"(acc));
           }
-          if (mc)
-            asm volatile(
-                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-                    su32(&empty[st])),
-                "h"(static_cast<unsigned short>(3))
-                : "memory");
-          else
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             su32(&empty[st]))
-                         : "memory");
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                           su32(&empty[st]))
+                       : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                          su32(&tfull[buf]))
@@ -539,7 +516,7 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
-  if (S > 1 || mc) {  // peers may still read this CTA's partial slots / multicast into its ring
+  if (S > 1) {  // peers may still read this CTA's partial slots
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -1225,14 +1202,8 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
     fprintf(stderr, "splitk N=%d K=%d M=%d: S=%d clusters=%d%s\n", a.N, a.K, a.M, sp.S, sp.clusters,
             use_sk ? " stream-K" : "");
   const std::int64_t a_rows = a.a_rows > 0 ? a.a_rows : (g_a_rows_capacity > a.M ? g_a_rows_capacity : a.M);
-  // Whole tiles, one per CTA, an even count that fits: pair the CTAs in
-  // clusters of two that share the activation tile (half each, multicast).
-  static const bool no_mc = getenv("IB2_NO_A_MULTICAST") != nullptr;  // diagnostics
-  const int mc = (!no_mc && !use_sk && sp.S == 1 && NT >= 16 && tiles % 2 == 0 && tiles <= g_sms &&
-                  2 * max_clusters(tc_splitk_kernel<NT, STAGES>, 2, L::TOTAL) >= tiles) ? 1 : 0;
-  if (mc) sp.clusters = tiles;
   const CUtensorMap& mw = cached_wmap(a.w, a.N, a.K, BM);
-  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, mc ? NT / 2 : NT);
+  const CUtensorMap& ma = cached_map(a.a, a_rows, a.K, NT);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(sp.clusters * sp.S);
   cfg.blockDim = dim3(256);
@@ -1240,14 +1211,14 @@ void launch_skinny(const GemmArgs& a, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = mc ? 2 : sp.S;
+  attr[0].val.clusterDim.x = sp.S;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_splitk_kernel<NT, STAGES>, mw, ma, a, sp.S, sk, mc));
+  IB2_CUDA(cudaLaunchKernelEx(&cfg, tc_splitk_kernel<NT, STAGES>, mw, ma, a, sp.S, sk));
 }
 
 bool skinny_ok(const GemmArgs& a) {
