@@ -484,6 +484,11 @@ __global__ void __launch_bounds__(256, 1) tc_splitk_kernel(const __grid_constant
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&tempty[buf])) : "memory");
       if (S == 1) continue;
       // Partials of this slot -> every rank; then reduce this rank's columns.
+      // Every writer fences at cluster scope before its warp's lanes < S
+      // signal the ranks (release by the signalling lane covers the warp's
+      // writes through __syncwarp as well; the explicit fence states it).
+      asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+      __syncwarp();
       if (lane < S) arrive_remote(map_to_rank(su32(&ready[slot]), lane));
       wait_cluster(&ready[slot], (seg / NS) & 1);
       const std::uint32_t local = su32(part) + row * 4;
