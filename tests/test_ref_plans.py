@@ -50,3 +50,17 @@ def test_reference_plans_match_product_c0(tmp_path, policy):
             flag_diff += 1
     assert shape_diff == 0
     assert flag_diff <= max(5, len(ref) // 1000), flag_diff
+
+
+def test_kept_iterations_equal_full_parse(tmp_path):
+    """The bench parses only the kept iterations' neighbourhoods of the event
+    log (oracle.ref_plans keep=...): same plans as a full parse."""
+    from oracle.ref_plans import plans_from_events, reference_schedule
+    summ, full = reference_schedule(C0_WORKLOAD, C0_COST, dict(policy="infercept"), workdir=str(tmp_path))
+    keep = {2, 331, 452, 9000, 18000, 18182}
+    with open(tmp_path / "ref_events.jsonl") as f:
+        kept = list(plans_from_events(f, keep))
+    assert [p["it"] for p in kept] == sorted(keep)
+    by_it = {p["it"]: p for p in full}
+    for p in kept:
+        assert p == by_it[p["it"]]
