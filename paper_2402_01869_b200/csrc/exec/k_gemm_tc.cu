@@ -1063,14 +1063,14 @@ void launch_tc_pair_bn(const GemmArgs& a, cudaStream_t s) {
   // Only for long k loops (K >= 8192: the MLP-down projections), where it
   // measured +11..14 %; at K <= 5120 it is neutral to -6 % and tiny GEMMs pay
   // the hand-off latency (C0: 0.20 -> 0.44 ms per iteration).
-  const bool use_sk = streamk_enabled(a, true) && !no_streamk && tiles % (g_sms / 2) != 0 &&
-                      (a.streamk_ok == 2 ? a.K / BK >= 2 : a.K / BK >= 128) && !getenv("IB2_PAIR_MAX");
-  const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
   // IB2_PAIR_MAX (diagnostics): cap the persistent grid, leaving SMs to
-  // kernels of another stream (split_batch experiments).
+  // kernels of another stream (split_batch experiments); no split tail then.
   static const int pair_cap = getenv("IB2_PAIR_MAX") ? atoi(getenv("IB2_PAIR_MAX")) : 0;
+  const bool use_sk = streamk_enabled(a, true) && !no_streamk && tiles % (g_sms / 2) != 0 &&
+                      (a.streamk_ok == 2 ? a.K / BK >= 2 : a.K / BK >= 128) && pair_cap == 0;
+  const StreamK sk = use_sk ? streamk_for(s) : StreamK{nullptr, nullptr, 0};
   const int max_pairs = pair_cap > 0 ? std::min(pair_cap, g_sms / 2) : g_sms / 2;
-  const int pairs = use_sk && max_pairs == g_sms / 2 ? g_sms / 2 : std::max(1, std::min(max_pairs, tiles));
+  const int pairs = use_sk ? g_sms / 2 : std::max(1, std::min(max_pairs, tiles));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(256);
