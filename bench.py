@@ -417,10 +417,10 @@ def run_b200(args):
         "gpu_launches": int(tot["kernel_launches"]),
         "clocks": clk,
     }
-    from oracle.ref_plans import REF_LIB
-    if world == 1 and not args.no_cpu_baseline and not os.path.exists(REF_LIB):
+    ref_lib = os.path.join(ROOT, "oracle", "_ref", "libinterceptsim.so")  # the cpu_baseline leg's checker
+    if world == 1 and not args.no_cpu_baseline and not os.path.exists(ref_lib):
         line["cpu_baseline"] = {"value": None, "unit": "req/s", "cores": os.cpu_count(), "kind": "reference",
-                                "sample": f"unavailable: {REF_LIB} not built"}
+                                "sample": f"unavailable: {ref_lib} not built"}
     elif world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(cfg, args, wins)
         line["cpu_baseline"] = {"value": cpu["value"], "unit": "req/s", "cores": cpu["cores"], "kind": "port",
