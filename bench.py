@@ -430,11 +430,12 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
-def cpu_forward_seconds(preset, layers_total, plans, reps=2):
+def cpu_forward_seconds(preset, layers_total, plans):
     """Seconds per iteration of the numpy fp32 oracle forward over `plans`
-    with all host threads: 1- and 2-layer models timed (reps each, after one
-    untimed warm-up), extrapolated to `layers_total` layers.  KV rows are
-    materialised with non-zero contents (real memory traffic)."""
+    with all host threads: each plan timed with a 1- and a 2-layer model
+    (after one untimed warm-up), extrapolated to `layers_total` layers, then
+    averaged.  KV rows are materialised with non-zero contents (real memory
+    traffic)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
     from oracle.forward import ForwardOracle
@@ -452,17 +453,18 @@ def cpu_forward_seconds(preset, layers_total, plans, reps=2):
                 kv.fill(np.float32(1e-3))
             fo._forward_only(plans[0])
             times = []
-            for _ in range(reps):
+            for pj in plans:
                 t = time.perf_counter()
-                for pj in plans:
-                    fo._forward_only(pj)
-                times.append((time.perf_counter() - t) / len(plans))
+                fo._forward_only(pj)
+                times.append(time.perf_counter() - t)
             per_layers[layers] = times
             del fo
-    t1, t2 = min(per_layers[1]), min(per_layers[2])
-    per_iter = t1 + (layers_total - 1) * max(t2 - t1, 0.0)
-    spread = max(max(v) / min(v) - 1.0 for v in per_layers.values())
-    return per_iter, dict(t1=t1, t2=t2, spread=spread, cores=cores, runs=per_layers)
+    per_plan = [a + (layers_total - 1) * max(b - a, 0.0) for a, b in zip(per_layers[1], per_layers[2])]
+    per_iter = sum(per_plan) / len(per_plan)
+    t1 = sum(per_layers[1]) / len(plans)
+    t2 = sum(per_layers[2]) / len(plans)
+    return per_iter, dict(t1=t1, t2=t2, cores=cores, per_iteration_s=[round(x, 3) for x in per_plan],
+                          runs={str(k): [round(x, 4) for x in v] for k, v in per_layers.items()})
 
 
 def cpu_full_trace_seconds(preset, plans):
@@ -514,7 +516,8 @@ def cpu_reference(cfg, args, wins):
     """The reference's CPU path on this host (see module docstring)."""
     from oracle.ref_plans import reference_schedule, run_reference as ref_run
     full = getattr(args, "full_trace", False)
-    keep = None if full else {s + 1 for s, _ in wins}  # event-log iteration numbers are 1-based
+    # every timed iteration of every window (event-log iteration numbers are 1-based)
+    keep = None if full else {s + 1 + j for s, c in wins for j in range(c)}
     with tempfile.TemporaryDirectory() as d:
         summ, plans = reference_schedule(cfg["workload"], cfg["cost"], RUN, keep=keep, workdir=d)
     t_sched = ref_run(cfg["workload"], cfg["cost"], RUN, None)["wall_s"] / summ["iterations"]
@@ -537,11 +540,12 @@ def cpu_reference(cfg, args, wins):
     return {"value": value, "s_per_iteration": per_iter, "cores": det["cores"], "iterations": summ["iterations"],
             "completed": summ["done_events"], "sched_us_per_iteration": t_sched * 1e6, "forward": det,
             "sample": (f"reference engine (oracle/_ref, whole trace: {int(summ['iterations'])} iterations, "
-                       f"{t_sched * 1e6:.1f} us/iteration) + numpy fp32 oracle forward of "
-                       f"{len(plans)} sampled iterations (first of each window; batches recovered from the "
-                       f"reference's event log) timed with 1 and 2 layers ({det['t1']:.2f} / {det['t2']:.2f} s, "
-                       f"run-to-run spread {det['spread'] * 100:.1f} %) and extrapolated to {cfg['layers']} layers: "
-                       f"{per_iter:.2f} s/iteration; EXTRAPOLATED, not a full-depth timed run")}
+                       f"{t_sched * 1e6:.1f} us/iteration) + numpy fp32 oracle forward of the "
+                       f"{len(plans)} timed iterations of the B200 arm's windows (batches recovered from the "
+                       f"reference's event log), each timed with 1 and 2 layers (mean {det['t1']:.2f} / "
+                       f"{det['t2']:.2f} s) and extrapolated to {cfg['layers']} layers: {per_iter:.2f} s/iteration "
+                       f"(per iteration {min(det['per_iteration_s']):.1f}-{max(det['per_iteration_s']):.1f} s); "
+                       f"EXTRAPOLATED, not a full-depth timed run")}
 
 
 def run_reference(args):
