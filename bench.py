@@ -459,7 +459,10 @@ def cpu_forward_seconds(preset, layers_total, plans):
                 times.append(time.perf_counter() - t)
             per_layers[layers] = times
             del fo
-    per_plan = [a + (layers_total - 1) * max(b - a, 0.0) for a, b in zip(per_layers[1], per_layers[2])]
+    if layers_total <= 2:  # the model itself was timed
+        per_plan = list(per_layers[layers_total])
+    else:
+        per_plan = [a + (layers_total - 1) * max(b - a, 0.0) for a, b in zip(per_layers[1], per_layers[2])]
     per_iter = sum(per_plan) / len(per_plan)
     t1 = sum(per_layers[1]) / len(plans)
     t2 = sum(per_layers[2]) / len(plans)
