@@ -33,9 +33,10 @@ session (plan upload from pinned memory and sampled-id read-back included).
 the reference engine (oracle/_ref, compiled from /root/reference) runs the
 whole trace; its event log with ledger snapshots gives each iteration's batch
 (oracle/ref_plans.py, no product code loaded); the numpy fp32 oracle forward
-(oracle/forward.py) of the sampled iterations, timed with all host threads
-(1- and 2-layer runs, extrapolated to the model's depth), plus the
-reference scheduler's own seconds per iteration, is its time per iteration.
+(oracle/forward.py) of the same timed iterations as the B200 arm, each timed
+with all host threads (1- and 2-layer runs, extrapolated to the model's
+depth), plus the reference scheduler's own seconds per iteration, is its time
+per iteration.  --full-trace (C0) times every iteration at full depth instead.
 """
 import argparse
 import json
