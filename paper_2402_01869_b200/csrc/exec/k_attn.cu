@@ -10,6 +10,7 @@
 //
 // K2 (chunk rows) lives in k_attn_chunk.cu (tcgen05 + TMEM + TMA).
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -17,7 +18,7 @@ namespace ib2 {
 
 namespace {
 
-constexpr int kSplit = 256;       // positions per K1 CTA
+constexpr int kSplit = 256;       // shortest positions per K1 CTA (partial buffers are sized for it)
 constexpr int kDecWarps = 4;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -34,7 +35,7 @@ __device__ __forceinline__ void h8_to_f32(const uint4& u, float* f) {
 // Occupancy: at head_dim 256 the unconstrained kernel takes 96 registers (5
 // CTAs per SM); capping it at 80 (6 CTAs per SM, 28 B of spills) measured
 // +2 % K1 bandwidth on the C1 window, a cap of 7 CTAs -4 % (profiles/r1j).
-template <int HD>
+template <int HD, int SPLIT = kSplit>
 __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn_kernel(
     const f16* __restrict__ qkv, const std::int32_t* __restrict__ drow, const RowDesc* __restrict__ rows,
     const f16* __restrict__ pool, std::int64_t layer_off, std::int64_t block_stride,
@@ -48,14 +49,14 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
   const int r = drow[dr];
   const RowDesc d = rows[r];
   const int ctx = d.pos + 1;
-  const int start = split * kSplit;
+  const int start = split * SPLIT;
   if (start >= ctx) return;
-  const int end = min(ctx, start + kSplit);
+  const int end = min(ctx, start + SPLIT);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = lane % LPT, grp = lane / LPT;
   const int D = H * HD;
 
-  __shared__ float s_score[kSplit];
+  __shared__ float s_score[SPLIT];
   __shared__ float s_red[kDecWarps];
   __shared__ float s_acc[kDecWarps][HD];
 
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(kDecWarps * 32, HD == 256 ? 6 : 1) decode_attn
   // order, so the result does not depend on which CTA is last) and re-arms
   // the counter: no separate combine launch, and the merge runs in K1's tail.
   __shared__ int s_last;
-  const int ns = (ctx + kSplit - 1) / kSplit;
+  const int ns = (ctx + SPLIT - 1) / SPLIT;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -189,11 +190,20 @@ template <int HD>
 void launch_decode_hd(const f16* qkv, const std::int32_t* drow, const RowDesc* rows, int n, const KvGeom& g,
                       int layer, int max_pos1, float* part_o, float* part_ml, f16* out,
                       std::int32_t* counters, cudaStream_t s) {
-  const int max_splits = (max_pos1 + kSplit - 1) / kSplit;
-  dim3 grid(max_splits, g.heads, n);
-  launch_pdl(decode_attn_kernel<HD>, grid, dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
-             layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, max_splits, part_o, part_ml,
-             out, counters);
+  // Positions per CTA: 512 at head dims <= 128, 256 at 256 (measured, profiles/r3i: C4 K1 0.99 vs
+  // 0.93 of the copy peak and 41.2 vs 42.0 ms per iteration; C1 K1 0.74 at 256 vs 0.70 at 512).
+  // IB2_K1_SPLIT = 256 / 512 / 1024 overrides (diagnostics).
+  static const int split_env = getenv("IB2_K1_SPLIT") ? atoi(getenv("IB2_K1_SPLIT")) : 0;
+  const int sp = (split_env == 256 || split_env == 512 || split_env == 1024) ? split_env : (HD == 256 ? 256 : 512);
+  const int ms = (max_pos1 + sp - 1) / sp;
+  auto go = [&](auto kernel) {
+    launch_pdl(kernel, dim3(ms, g.heads, n), dim3(kDecWarps * 32), 0, s, qkv, drow, rows, g.pool,
+               layer * g.layer_stride(), g.block_stride(), g.table, g.max_lblocks, g.heads, ms, part_o, part_ml, out,
+               counters);
+  };
+  if (sp == 256) go(decode_attn_kernel<HD, 256>);
+  else if (sp == 512) go(decode_attn_kernel<HD, 512>);
+  else go(decode_attn_kernel<HD, 1024>);
   IB2_LAUNCH_CHECK();
 }
 
